@@ -1,0 +1,222 @@
+// fwa_api.cu — the C-ABI (include/fwa.h): validation, kernel selection, errors.
+//
+// Validation mirrors the reference's checks and their order so the Python
+// layer can raise the same exception classes:
+//   TileConfig.__post_init__      flash.py:49-55   -> FWA_ERR_INVALID_RANGE
+//   TileConfig.chunk_width        flash.py:57-66   -> FWA_ERR_SHAPE
+//   _check_qkv_2d / dO shape      flash.py:322-327, :202-203 -> FWA_ERR_SHAPE
+//   _check_budget (before work)   flash.py:98-103  -> FWA_ERR_CAPACITY
+#include <math.h>
+#include <stdio.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+
+#include "fwa_common.cuh"
+
+namespace fwa {
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+int check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return FWA_OK;
+  return fail(FWA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void count_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+struct DevInfo {
+  int sm = 0;
+  int64_t l2 = 0;
+  size_t smem_optin = 0;
+};
+DevInfo query_dev() {
+  DevInfo d;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return d;
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) d.sm = v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess) d.l2 = v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess)
+    d.smem_optin = (size_t)v;
+  return d;
+}
+const DevInfo& dev_info() {
+  // per-process cache; the library targets one device per process (torchrun model)
+  static DevInfo info = query_dev();
+  return info;
+}
+}  // namespace
+
+int device_sm_count() { return dev_info().sm > 0 ? dev_info().sm : 148; }
+int64_t device_l2_bytes() { return dev_info().l2; }
+size_t device_max_smem_optin() {
+  return dev_info().smem_optin ? dev_info().smem_optin : (size_t)227 * 1024;
+}
+
+namespace {
+
+int64_t paper_peak(int L, int C, int cw, int eb, bool bwd) {
+  return ((bwd ? 2 : 1) * (int64_t)L * L + 2 * (int64_t)L * cw) * eb;
+}
+
+// Reference-ordered validation; fills g and picks kernels. No device work.
+int validate(const fwa_desc* d, Geom* g, bool need_mask_windows_if_mask, const float* mask) {
+  if (!d) return fail(FWA_ERR_SHAPE, "null descriptor");
+  if (d->dtype != FWA_F32 && d->dtype != FWA_F16 && d->dtype != FWA_BF16)
+    return fail(FWA_ERR_INVALID_RANGE, "dtype must be FWA_F32, FWA_F16 or FWA_BF16");
+  if (d->chunks < 1)
+    return fail(FWA_ERR_INVALID_RANGE, "chunk count must be >= 1, got " + std::to_string(d->chunks));
+  if (!isfinite(d->scale) || d->scale <= 0.f)
+    return fail(FWA_ERR_INVALID_RANGE, "scale must be finite and > 0");
+  if (d->num_windows < 1 || d->heads < 1 || d->seq_len < 1 || d->head_dim < 1)
+    return fail(FWA_ERR_SHAPE, "N, heads, L and d must all be >= 1 (got N=" +
+                                   std::to_string(d->num_windows) + ", h=" +
+                                   std::to_string(d->heads) + ", L=" + std::to_string(d->seq_len) +
+                                   ", d=" + std::to_string(d->head_dim) + ")");
+  const int C = d->head_dim, r = d->chunks;
+  if (r > C)
+    return fail(FWA_ERR_SHAPE, "chunk count " + std::to_string(r) + " exceeds feature count " +
+                                   std::to_string(C));
+  const int cw = (C + r - 1) / r;
+  if ((int64_t)cw * (r - 1) >= C)
+    return fail(FWA_ERR_SHAPE, "chunk count " + std::to_string(r) +
+                                   " leaves an empty chunk for " + std::to_string(C) + " features");
+  if (need_mask_windows_if_mask && mask && d->mask_windows < 1)
+    return fail(FWA_ERR_SHAPE, "mask given but mask_windows < 1");
+  if (d->kernel < FWA_KERNEL_AUTO || d->kernel > FWA_KERNEL_TC)
+    return fail(FWA_ERR_INVALID_RANGE, "unknown kernel selector");
+  g->units = d->num_windows * d->heads;
+  g->heads = d->heads;
+  g->L = d->seq_len;
+  g->d = d->head_dim;
+  g->scale = d->scale;
+  g->mask_windows = mask ? d->mask_windows : 1;
+  return FWA_OK;
+}
+
+int pick_fwd(const fwa_desc* d, const Geom& g, int* kernel, size_t* smem, int* tmem) {
+  const bool tc_ok = tc_fwd_supported(g, d->dtype);
+  if (d->kernel == FWA_KERNEL_TC && !tc_ok)
+    return fail(FWA_ERR_CAPACITY, "tcgen05 forward does not support this shape/dtype (L=" +
+                                      std::to_string(g.L) + ", d=" + std::to_string(g.d) + ")");
+  if (tc_ok && d->kernel != FWA_KERNEL_GENERIC) {
+    *kernel = FWA_KERNEL_TC;
+    *smem = tc_fwd_smem(g, d->dtype);
+    *tmem = tc_fwd_tmem_cols(g);
+    return FWA_OK;
+  }
+  *kernel = FWA_KERNEL_GENERIC;
+  *smem = fwd_generic_smem(g);
+  *tmem = 0;
+  if (*smem > device_max_smem_optin())
+    return fail(FWA_ERR_CAPACITY, "forward pass needs " + std::to_string(*smem) +
+                                      " bytes of shared memory, device provides " +
+                                      std::to_string(device_max_smem_optin()));
+  return FWA_OK;
+}
+
+int pick_bwd(const fwa_desc* d, const Geom& g, int* kernel, size_t* smem, int* tmem) {
+  if (d->kernel == FWA_KERNEL_TC)
+    return fail(FWA_ERR_CAPACITY, "tcgen05 backward is not available for this shape");
+  *kernel = FWA_KERNEL_GENERIC;
+  *smem = bwd_generic_smem(g);
+  *tmem = 0;
+  if (*smem > device_max_smem_optin())
+    return fail(FWA_ERR_CAPACITY, "backward pass needs " + std::to_string(*smem) +
+                                      " bytes of shared memory, device provides " +
+                                      std::to_string(device_max_smem_optin()));
+  return FWA_OK;
+}
+
+}  // namespace
+}  // namespace fwa
+
+using namespace fwa;
+
+extern "C" const char* fwa_last_error(void) { return g_last_error.c_str(); }
+extern "C" int fwa_abi_version(void) { return FWA_ABI_VERSION; }
+extern "C" int64_t fwa_launch_count(void) { return g_launches.load(); }
+
+extern "C" int fwa_device_info(int32_t* sm_count, int64_t* l2_bytes) {
+  if (sm_count) *sm_count = device_sm_count();
+  if (l2_bytes) *l2_bytes = device_l2_bytes();
+  return FWA_OK;
+}
+
+extern "C" int fwa_footprint(const fwa_desc* desc, fwa_footprint_t* out) {
+  Geom g;
+  int rc = validate(desc, &g, false, nullptr);
+  if (rc) return rc;
+  if (!out) return fail(FWA_ERR_SHAPE, "null footprint output");
+  const int eb = elem_bytes(desc->dtype);
+  const int cw = (g.d + desc->chunks - 1) / desc->chunks;
+  out->paper_peak_fwd = paper_peak(g.L, g.d, cw, eb, false);
+  out->paper_peak_bwd = paper_peak(g.L, g.d, cw, eb, true);
+  const int64_t lcd = g.units * g.L * (int64_t)g.d * eb;
+  out->hbm_bytes_fwd = 4 * lcd;
+  out->hbm_bytes_bwd = 7 * lcd;
+  size_t smem = 0;
+  int kern = 0, tmem = 0;
+  rc = pick_fwd(desc, g, &kern, &smem, &tmem);
+  if (rc) return rc;
+  out->kernel_fwd = kern;
+  out->smem_bytes_fwd = (int64_t)smem;
+  out->tmem_cols_fwd = tmem;
+  rc = pick_bwd(desc, g, &kern, &smem, &tmem);
+  if (rc) return rc;
+  out->kernel_bwd = kern;
+  out->smem_bytes_bwd = (int64_t)smem;
+  out->tmem_cols_bwd = tmem;
+  return FWA_OK;
+}
+
+extern "C" int fwa_fwd(const fwa_desc* desc, const void* q, const void* k, const void* v,
+                       const float* bias, const float* mask, void* o, void* stream) {
+  Geom g;
+  int rc = validate(desc, &g, true, mask);
+  if (rc) return rc;
+  if (!q || !k || !v || !o) return fail(FWA_ERR_SHAPE, "null q/k/v/o pointer");
+  int kern = 0, tmem = 0;
+  size_t smem = 0;
+  rc = pick_fwd(desc, g, &kern, &smem, &tmem);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (kern == FWA_KERNEL_TC) return launch_fwd_tc(g, desc->dtype, q, k, v, bias, mask, o, s);
+  return launch_fwd_generic(g, desc->dtype, q, k, v, bias, mask, o, s);
+}
+
+extern "C" size_t fwa_bwd_workspace_bytes(const fwa_desc* desc, int want_dbias) {
+  Geom g;
+  if (validate(desc, &g, false, nullptr)) return 0;
+  if (!want_dbias) return 0;
+  return (size_t)bwd_generic_grid(g) * g.heads * g.L * g.L * sizeof(float);
+}
+
+extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const void* v,
+                       const void* dout, const float* bias, const float* mask, void* dq, void* dk,
+                       void* dv, float* dbias, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  Geom g;
+  int rc = validate(desc, &g, true, mask);
+  if (rc) return rc;
+  if (!q || !k || !v || !dout || !dq || !dk || !dv)
+    return fail(FWA_ERR_SHAPE, "null q/k/v/dO/dq/dk/dv pointer");
+  int kern = 0, tmem = 0;
+  size_t smem = 0;
+  rc = pick_bwd(desc, g, &kern, &smem, &tmem);
+  if (rc) return rc;
+  const size_t need = fwa_bwd_workspace_bytes(desc, dbias != nullptr);
+  if (need && (!workspace || workspace_bytes < need))
+    return fail(FWA_ERR_CAPACITY, "backward workspace needs " + std::to_string(need) +
+                                      " bytes, got " + std::to_string(workspace_bytes));
+  return launch_bwd_generic(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
+                            (float*)workspace, (cudaStream_t)stream);
+}

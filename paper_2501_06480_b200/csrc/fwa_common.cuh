@@ -1,0 +1,77 @@
+// fwa_common.cuh — shared device/host helpers for libfwa (sm_100a only).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/fwa.h"
+
+namespace fwa {
+
+// ---- dtype traits ---------------------------------------------------------
+template <typename T> struct DT;
+template <> struct DT<float> {
+  static constexpr int id = FWA_F32;
+  __device__ __forceinline__ static float to_f(float x) { return x; }
+  __device__ __forceinline__ static float from_f(float x) { return x; }
+};
+template <> struct DT<__half> {
+  static constexpr int id = FWA_F16;
+  __device__ __forceinline__ static float to_f(__half x) { return __half2float(x); }
+  __device__ __forceinline__ static __half from_f(float x) { return __float2half_rn(x); }
+};
+template <> struct DT<__nv_bfloat16> {
+  static constexpr int id = FWA_BF16;
+  __device__ __forceinline__ static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+  __device__ __forceinline__ static __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
+};
+
+inline int elem_bytes(int dtype) { return dtype == FWA_F32 ? 4 : 2; }
+
+// ---- host-side error plumbing ---------------------------------------------
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int check_cuda(cudaError_t e, const char* what);
+void count_launch(int64_t n = 1);
+
+// Problem geometry shared by the kernels.
+struct Geom {
+  int64_t units;   // N * h
+  int32_t heads;
+  int32_t L;
+  int32_t d;
+  float scale;
+  int32_t mask_windows;
+};
+
+// ---- kernel launchers (defined in the .cu files) --------------------------
+int launch_fwd_generic(const Geom& g, int dtype, const void* q, const void* k,
+                       const void* v, const float* bias, const float* mask,
+                       void* o, cudaStream_t s);
+size_t fwd_generic_smem(const Geom& g);
+
+int launch_bwd_generic(const Geom& g, int dtype, const void* q, const void* k,
+                       const void* v, const void* dout, const float* bias,
+                       const float* mask, void* dq, void* dk, void* dv,
+                       float* dbias, float* ws, cudaStream_t s);
+size_t bwd_generic_smem(const Geom& g);
+bool bwd_generic_fits(const Geom& g);
+int bwd_generic_grid(const Geom& g);
+
+// tcgen05 / TMA forward (fwa_tc_fwd.cu)
+bool tc_fwd_supported(const Geom& g, int dtype);
+size_t tc_fwd_smem(const Geom& g, int dtype);
+int tc_fwd_tmem_cols(const Geom& g);
+int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k,
+                  const void* v, const float* bias, const float* mask, void* o,
+                  cudaStream_t s);
+
+int device_sm_count();
+int64_t device_l2_bytes();
+size_t device_max_smem_optin();
+
+}  // namespace fwa

@@ -1,0 +1,127 @@
+"""CPU-only tests: host logic, C-ABI exports and validation (no kernel launches)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2501_06480_b200 as fw
+from paper_2501_06480_b200 import _native as nat
+from paper_2501_06480_b200.tiling import backward_report, forward_report, merge_reports
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    with open(os.path.join(ROOT, "include", "fwa.h")) as f:
+        header = f.read()
+    declared = set(re.findall(r"\b(fwa_[a-z_0-9]+)\s*\(", header))
+    assert declared, "no declarations parsed"
+    lib = nat.load()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(nat.EXPORTED_SYMBOLS)
+    assert lib.fwa_abi_version() == 1
+
+
+def test_tileconfig_matches_reference_rules(golden):
+    assert fw.TileConfig(r=4).chunk_width(64) == 16
+    assert fw.TileConfig(r=4).chunk_width(10) == 3
+    assert fw.TileConfig(r=4).chunk_spans(10) == [(0, 3), (3, 6), (6, 9), (9, 10)]
+    with pytest.raises(fw.InvalidRangeError):
+        fw.TileConfig(r=0)
+    with pytest.raises(fw.InvalidRangeError):
+        fw.TileConfig(r=1, elem_bytes=2)
+    with pytest.raises(fw.InvalidRangeError):
+        fw.TileConfig(r=1, scale=-1.0)
+    with pytest.raises(fw.ShapeError):
+        fw.TileConfig(r=5).chunk_width(4)
+    with pytest.raises(fw.ShapeError):
+        fw.TileConfig(r=3).chunk_width(4)
+    scalars, _ = golden
+    for p in scalars["peaks"]:
+        cfg = fw.TileConfig(r=p["r"], elem_bytes=p["elem_bytes"])
+        assert fw.peak_sram_forward(p["L"], p["C"], cfg) == p["fwd"]
+        assert fw.peak_sram_backward(p["L"], p["C"], cfg) == p["bwd"]
+
+
+def test_reports_merge_like_reference(golden):
+    scalars, _ = golden
+    b = scalars["batched70"]
+    reps = [forward_report(1, 64, 64, 24576) for _ in range(16)]
+    m = merge_reports(reps)
+    assert m.loads == b["loads"] and m.stores == b["stores"] and m.peak_sram_bytes == b["peak"]
+    for case in scalars["grid"][:10]:
+        L, C = case["L"], case["C"]
+        br = backward_report(1, L, C, case["bwd_peak"])
+        assert br.loads == case["bwd_loads"] and br.stores == case["bwd_stores"]
+
+
+def test_capacity_and_shape_errors_raised_before_device_use():
+    # No GPU here: these must fail in validation, never reach CUDA.
+    q = np.zeros((1024, 32))
+    with pytest.raises(fw.CapacityError, match="131072"):
+        fw.flash_forward(q, q, q, fw.TileConfig(r=2), fw.ScratchpadArena())
+    with pytest.raises(fw.ShapeError):
+        fw.flash_forward(np.zeros((2, 4)), np.zeros((2, 4)), np.zeros((2, 6)),
+                         fw.TileConfig(r=1), fw.ScratchpadArena())
+    with pytest.raises(fw.ContextError):
+        fw.flash_backward(None, np.zeros((2, 2)), fw.ScratchpadArena())
+    q4 = np.zeros((2, 2, 64, 64))
+    with pytest.raises(fw.CapacityError, match=r"slice \(b=0, head=0\)"):
+        fw.batched_flash_forward(q4, q4, q4, fw.TileConfig(r=1), [fw.ScratchpadArena(1024)])
+    with pytest.raises(fw.InvalidRangeError):
+        fw.batched_flash_forward(q4, q4, q4, fw.TileConfig(r=1), [])
+    with pytest.raises(fw.PartitionError):
+        fw.WindowConfig(H=10, W=10, C=3, k=3)
+    with pytest.raises(fw.ShapeError):
+        fw.WindowConfig(H=0, W=4, C=1, k=2)
+
+
+def _desc(**kw):
+    base = dict(N=4, h=3, L=49, d=32, dtype=1, scale=1.0, chunks=2, mask_windows=0, kernel="auto")
+    base.update(kw)
+    return fw.ops.make_desc(base["N"], base["h"], base["L"], base["d"], base["dtype"],
+                            base["scale"], base["chunks"], base["mask_windows"], base["kernel"])
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(), 0),
+    (dict(N=0), 1),
+    (dict(L=0), 1),
+    (dict(chunks=0), 3),
+    (dict(chunks=33), 1),
+    (dict(d=4, chunks=3), 1),   # ceil(4/3)=2 leaves an empty chunk
+    (dict(scale=float("nan")), 3),
+    (dict(scale=-1.0), 3),
+    (dict(dtype=7), 3),
+])
+def test_c_abi_validation_codes(kw, status):
+    lib = nat.load()
+    fp = nat.FwaFootprint()
+    d = _desc(**kw)
+    assert lib.fwa_footprint(ctypes.byref(d), ctypes.byref(fp)) == status
+    if status:
+        assert lib.fwa_last_error()
+
+
+def test_c_abi_rejects_null_pointers_without_launching():
+    lib = nat.load()
+    d = _desc()
+    before = lib.fwa_launch_count()
+    assert lib.fwa_fwd(ctypes.byref(d), None, None, None, None, None, None, None) == 1
+    assert lib.fwa_launch_count() == before
+
+
+def test_shard_ranges_cover_batch_exactly():
+    from paper_2501_06480_b200.shard import shard_images
+
+    for B, G in [(128, 1), (128, 2), (128, 8), (7, 3), (1, 2)]:
+        shards = [shard_images(B, 64, r, G) for r in range(G)]
+        assert shards[0].image_begin == 0 and shards[-1].image_end == B
+        for a, b in zip(shards, shards[1:]):
+            assert a.image_end == b.image_begin
+        assert sum(s.windows for s in shards) == B * 64
+        assert all(s.window_begin % 64 == 0 for s in shards)  # mask index n % nW preserved
