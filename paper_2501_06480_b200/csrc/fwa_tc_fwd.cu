@@ -1,12 +1,377 @@
-// fwa_tc_fwd.cu — tcgen05/TMA forward (placeholder until the kernel lands).
+// fwa_tc_fwd.cu — Flash Window Attention forward on tcgen05 + TMA (sm_100a).
+//
+// Algorithm 1 of the paper (reference flash.py:141-184) for
+// f16/bf16, L <= 64, d in {16, 32, 64}, without bias/mask (those shapes take
+// the generic kernel for now):
+//
+//   * A tile = 128 rows = two (window, head) units, each padded to 64 rows.
+//     TMA loads Q, K, V with a 3-D tensor map (d, L, units) and box (d, 64, 2):
+//     rows L..63 are out of bounds and arrive as zeros, so L = 49 needs no
+//     host padding, and the swizzled smem image is exactly the UMMA
+//     K-major (Q, K) / MN-major (V) canonical layout.
+//   * S = Q K^T: one tcgen05.mma chain (M=128, N=128, K=d) into TMEM columns
+//     [0,128). Only the two diagonal 64x64 blocks are used.
+//   * Softmax: 4 warps, one thread per row (TMEM lane = row): tcgen05.ld of the
+//     row's own 64-column block, masked max over the L valid keys, ex2, row
+//     sum; P (unnormalised, f16/bf16) goes to shared memory in the SW128
+//     K-major layout. The two off-diagonal 64x64 blocks of P share one zeroed
+//     8 KB region (24 KB instead of 32 KB).
+//   * O = P V: tcgen05.mma (M=128, N=d, K=128) into TMEM columns [128,128+d).
+//   * Epilogue: tcgen05.ld, scale by 1/rowsum, convert, swizzled staging,
+//     TMA store with the same 3-D map (rows >= L are clipped by the map).
+//
+// Warp roles (192 threads, 2 CTAs per SM, persistent over tiles):
+//   warp 0: TMA producer, warp 1: TMEM allocator + MMA issuer,
+//   warps 2-5: softmax + epilogue (warp w owns TMEM lanes 32*(w%4)..+31).
+// HBM is touched once per tensor: Q, K, V read once, O written once.
+#include <cuda.h>
+#include <math.h>
+
+#include <algorithm>
+#include <mutex>
+
 #include "fwa_common.cuh"
+#include "fwa_sm100.cuh"
 
 namespace fwa {
-bool tc_fwd_supported(const Geom&, int) { return false; }
-size_t tc_fwd_smem(const Geom&, int) { return 0; }
-int tc_fwd_tmem_cols(const Geom&) { return 0; }
-int launch_fwd_tc(const Geom&, int, const void*, const void*, const void*, const float*,
-                  const float*, void*, cudaStream_t) {
-  return fail(FWA_ERR_CAPACITY, "tcgen05 forward not built");
+namespace {
+
+using namespace sm100;
+
+constexpr int kThreads = 192;
+constexpr int kTileRows = 128;     // MMA M
+constexpr int kUnitRows = 64;      // rows per packed unit
+constexpr int kPBytes = 24 * 1024; // P tile with the shared zero block
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemO = 128;   // O accumulator column offset
+
+template <int D>
+struct Cfg {
+  static constexpr int kRowBytes = D * 2;
+  static constexpr int kTileBytes = kTileRows * kRowBytes;            // one of Q/K/V per stage
+  static constexpr int kStages = D <= 16 ? 4 : (D <= 32 ? 2 : 2);
+  static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);  // UMMA layout code
+  static constexpr int kSmem = 1024 /*align slack*/ + kStages * 3 * kTileBytes + kPBytes +
+                               2 * kTileBytes /*O staging*/ + 256 /*barriers*/;
+  static constexpr int kChunks = kRowBytes / 16;  // 16-byte chunks per row
+};
+
+struct SmemBarriers {
+  uint64_t full[4];
+  uint64_t empty[4];
+  uint64_t s_full, s_empty, p_full, pv_done;
+  uint32_t tmem_base;
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads, 2)
+fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+              int n_tiles, int L, float scale_log2) {
+  using C = Cfg<D>;
+  constexpr bool kBF16 = DT<T>::id == FWA_BF16;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + C::kStages * C::kTileBytes;
+  uint8_t* sV = sK + C::kStages * C::kTileBytes;
+  uint8_t* sP = sV + C::kStages * C::kTileBytes;
+  uint8_t* sO = sP + kPBytes;
+  SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(sO + 2 * C::kTileBytes);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // zero P (the off-diagonal block must stay zero for the whole kernel)
+  for (int i = threadIdx.x; i < kPBytes / 16; i += kThreads)
+    reinterpret_cast<uint4*>(sP)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&bars->full[s], 1);
+      mbar_init(&bars->empty[s], 1);
+    }
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->s_empty, 128);
+    mbar_init(&bars->p_full, 128);
+    mbar_init(&bars->pv_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_o);
+  }
+  if (warp == 1) tmem_alloc(&bars->tmem_base, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  const int n_local = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int i = 0; i < n_local; ++i) {
+        const int tile = blockIdx.x + i * gridDim.x;
+        const int st = i % C::kStages;
+        const uint32_t round = i / C::kStages;
+        mbar_wait(&bars->empty[st], (round & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->full[st], 3 * C::kTileBytes);
+        tma_load_3d(sQ + st * C::kTileBytes, &tm_q, &bars->full[st], 0, 0, 2 * tile, pol);
+        tma_load_3d(sK + st * C::kTileBytes, &tm_k, &bars->full[st], 0, 0, 2 * tile, pol);
+        tma_load_3d(sV + st * C::kTileBytes, &tm_v, &bars->full[st], 0, 0, 2 * tile, pol);
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0 && n_local > 0) {
+      constexpr uint32_t idS = make_idesc_f16(kBF16, 128, 128, false, false);
+      constexpr uint32_t idO = make_idesc_f16(kBF16, 128, D, false, true);
+      constexpr uint32_t sbo_qk = 8 * C::kRowBytes;  // 8-row core-matrix group stride
+      auto issue_S = [&](int i) {
+        const int st = i % C::kStages;
+        const uint32_t q0 = smem_u32(sQ + st * C::kTileBytes);
+        const uint32_t k0 = smem_u32(sK + st * C::kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t a = make_sdesc(q0 + kk * 32, 16, sbo_qk, C::kSwz);
+          const uint64_t b = make_sdesc(k0 + kk * 32, 16, sbo_qk, C::kSwz);
+          mma_f16_ss(tmem, a, b, idS, kk > 0);
+        }
+        mma_commit(&bars->s_full);
+      };
+      mbar_wait(&bars->full[0], 0);
+      tc_fence_after();
+      issue_S(0);
+      for (int i = 0; i < n_local; ++i) {
+        const int st = i % C::kStages;
+        // O = P V once softmax has written P(i)
+        mbar_wait(&bars->p_full, i & 1);
+        tc_fence_after();
+        const uint32_t p0 = smem_u32(sP);
+        const uint32_t v0 = smem_u32(sV + st * C::kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t pa = p0 + (kk >> 2) * 8192 + (kk & 3) * 32;
+          const uint64_t a = make_sdesc(pa, 16, 1024, 2 /*SW128*/);
+          const uint64_t b = make_sdesc(v0 + kk * 16 * C::kRowBytes, C::kTileBytes,
+                                        8 * C::kRowBytes, C::kSwz);
+          mma_f16_ss(tmem + kTmemO, a, b, idO, kk > 0);
+        }
+        mma_commit(&bars->pv_done);
+        mma_commit(&bars->empty[st]);
+        if (i + 1 < n_local) {
+          const int st1 = (i + 1) % C::kStages;
+          mbar_wait(&bars->full[st1], ((i + 1) / C::kStages) & 1);
+          mbar_wait(&bars->s_empty, i & 1);
+          tc_fence_after();
+          issue_S(i + 1);
+        }
+      }
+    }
+  } else {
+    // ===================== softmax + epilogue (warps 2..5) =====================
+    const int q = warp & 3;               // TMEM lane quarter
+    const int row = q * 32 + lane;        // tile row = TMEM lane
+    const int ul = row >> 6;              // unit within the tile
+    const int r_in = row & 63;            // row within the unit
+    const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+    const uint32_t pswz = (uint32_t)(r_in & 7);
+    uint8_t* prow = sP + ul * 8192 + (row >> 3) * 1024 + (row & 7) * 128;
+    const bool leader = (threadIdx.x == 64);
+    for (int i = 0; i < n_local; ++i) {
+      const int tile = blockIdx.x + i * gridDim.x;
+      mbar_wait(&bars->s_full, i & 1);
+      tc_fence_after();
+      uint32_t s[64];
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        tmem_ld16(tmem + t_lane + ul * 64 + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&s[g * 16]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars->s_empty);
+      // masked row max over the L valid keys
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if (j < L) mx = fmaxf(mx, __uint_as_float(s[j]));
+      const float mxs = mx * scale_log2;
+      float sum = 0.f;
+      uint32_t pk[32];
+#pragma unroll
+      for (int j = 0; j < 64; j += 2) {
+        const float p0 = j < L ? ex2(fmaf(__uint_as_float(s[j]), scale_log2, -mxs)) : 0.f;
+        const float p1 = j + 1 < L ? ex2(fmaf(__uint_as_float(s[j + 1]), scale_log2, -mxs)) : 0.f;
+        if constexpr (kBF16) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+          const float2 back = __bfloat1622float2(h2);
+          sum += back.x + back.y;
+          pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+        } else {
+          __half2 h2 = __floats2half2_rn(p0, p1);
+          const float2 back = __half22float2(h2);
+          sum += back.x + back.y;
+          pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+      }
+      // P(i) -> smem (SW128 K-major). PV(i-1) finished reading P: we waited pv_done(i-1).
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4 v = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        *reinterpret_cast<uint4*>(prow + ((c ^ pswz) << 4)) = v;
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars->p_full);
+      // ---- epilogue ----
+      mbar_wait(&bars->pv_done, i & 1);
+      tc_fence_after();
+      uint32_t o[D];
+#pragma unroll
+      for (int g = 0; g < D / 16; ++g)
+        tmem_ld16(tmem + t_lane + kTmemO + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&o[g * 16]));
+      tmem_wait_ld();
+      tc_fence_before();
+      const float inv = 1.f / sum;
+      uint32_t ob[D / 2];
+#pragma unroll
+      for (int j = 0; j < D; j += 2) {
+        const float a = __uint_as_float(o[j]) * inv, b = __uint_as_float(o[j + 1]) * inv;
+        if constexpr (kBF16) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+          ob[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+        } else {
+          __half2 h2 = __floats2half2_rn(a, b);
+          ob[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+      }
+      uint8_t* stg = sO + (i & 1) * C::kTileBytes;
+      if (leader) bulk_wait_read<1>();
+      named_sync(1, 128);
+      uint8_t* orow = stg + row * C::kRowBytes;
+      const uint32_t oswz = (uint32_t)((row * C::kRowBytes) >> 7) & (C::kChunks - 1);
+#pragma unroll
+      for (int c = 0; c < C::kChunks; ++c) {
+        uint4 v = make_uint4(ob[4 * c], ob[4 * c + 1], ob[4 * c + 2], ob[4 * c + 3]);
+        *reinterpret_cast<uint4*>(orow + ((c ^ oswz) << 4)) = v;
+      }
+      fence_proxy_async_smem();
+      named_sync(2, 128);
+      if (leader) {
+        tma_store_3d(&tm_o, stg, 0, 0, 2 * tile);
+        bulk_commit();
+      }
+    }
+    if (leader) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, kTmemCols);
 }
+
+// ---- host side ---------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+int encode_units_map(CUtensorMap* m, const void* ptr, int dtype, int64_t units, int L, int d) {
+  EncodeFn enc = get_encode();
+  if (!enc) return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t gdim[3] = {(cuuint64_t)d, (cuuint64_t)L, (cuuint64_t)units};
+  const cuuint64_t gstride[2] = {(cuuint64_t)d * 2, (cuuint64_t)L * d * 2};
+  const cuuint32_t box[3] = {(cuuint32_t)d, (cuuint32_t)kUnitRows, 2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapSwizzle swz = d == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : d == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = enc(m, dtype == FWA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   3, const_cast<void*>(ptr), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return FWA_OK;
+}
+
+template <typename T, int D>
+int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
+             cudaStream_t s) {
+  CUtensorMap mq, mk, mv, mo;
+  int rc;
+  if ((rc = encode_units_map(&mq, q, dtype, g.units, g.L, g.d))) return rc;
+  if ((rc = encode_units_map(&mk, k, dtype, g.units, g.L, g.d))) return rc;
+  if ((rc = encode_units_map(&mv, v, dtype, g.units, g.L, g.d))) return rc;
+  if ((rc = encode_units_map(&mo, o, dtype, g.units, g.L, g.d))) return rc;
+  auto kern = fwd_tc_kernel<T, D>;
+  constexpr int smem = Cfg<D>::kSmem;
+  static bool attr_done = false;
+  if (!attr_done) {
+    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                    "cudaFuncSetAttribute(fwd_tc)");
+    if (rc) return rc;
+    attr_done = true;
+  }
+  const int n_tiles = (int)((g.units + 1) / 2);
+  const int per_sm = (2 * (smem + 1024) <= 228 * 1024) ? 2 : 1;
+  const int grid = std::max(1, std::min(n_tiles, device_sm_count() * per_sm));
+  const float scale_log2 = g.scale * 1.4426950408889634f;
+  kern<<<grid, kThreads, smem, s>>>(mq, mk, mv, mo, n_tiles, g.L, scale_log2);
+  count_launch();
+  return check_cuda(cudaGetLastError(), "fwd_tc_kernel launch");
+}
+
+}  // namespace
+
+bool tc_fwd_supported(const Geom& g, int dtype, bool bias_or_mask) {
+  if (bias_or_mask) return false;  // bias/mask shapes run on the generic kernel for now
+  if (dtype != FWA_F16 && dtype != FWA_BF16) return false;
+  if (g.L < 1 || g.L > kUnitRows) return false;
+  if (g.d != 16 && g.d != 32 && g.d != 64) return false;
+  if (g.units > (int64_t)1 << 31) return false;
+  return true;
+}
+
+size_t tc_fwd_smem(const Geom& g, int) {
+  return g.d == 16 ? Cfg<16>::kSmem : g.d == 32 ? Cfg<32>::kSmem : Cfg<64>::kSmem;
+}
+
+int tc_fwd_tmem_cols(const Geom&) { return (int)kTmemCols; }
+
+int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                  const float* bias, const float* mask, void* o, cudaStream_t s) {
+  if (bias || mask) return fail(FWA_ERR_CAPACITY, "tcgen05 forward: bias/mask not supported yet");
+  const bool bf = dtype == FWA_BF16;
+  switch (g.d) {
+    case 16: return bf ? launch_t<__nv_bfloat16, 16>(g, dtype, q, k, v, o, s)
+                       : launch_t<__half, 16>(g, dtype, q, k, v, o, s);
+    case 32: return bf ? launch_t<__nv_bfloat16, 32>(g, dtype, q, k, v, o, s)
+                       : launch_t<__half, 32>(g, dtype, q, k, v, o, s);
+    case 64: return bf ? launch_t<__nv_bfloat16, 64>(g, dtype, q, k, v, o, s)
+                       : launch_t<__half, 64>(g, dtype, q, k, v, o, s);
+  }
+  return fail(FWA_ERR_CAPACITY, "tcgen05 forward: unsupported head_dim");
+}
+
 }  // namespace fwa

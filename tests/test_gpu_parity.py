@@ -39,9 +39,11 @@ FWD_CASES = [
 
 @pytest.mark.parametrize("dt", ["f32", "f16", "bf16"])
 @pytest.mark.parametrize("N,h,L,d", FWD_CASES)
-@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("kernel", ["auto", "generic", "tc"])
 def test_forward_matches_oracle(dt, N, h, L, d, kernel):
     dtype = DTYPES[dt]
+    if kernel == "tc" and ops.footprint(N, h, L, d, dtype)["kernel_fwd"] != "tc":
+        pytest.skip("shape/dtype not on the tcgen05 path")
     (q, k, v), (qh, kh, vh) = draw(9000 + 100 * L + d, (N, h, L, d), 3, dtype)
     for scale in (1.0, d ** -0.5):
         o = ops.attention_forward(q, k, v, scale, kernel=kernel)
@@ -219,6 +221,37 @@ def test_autograd_matches_torch_reference():
     assert (o - ref).abs().max().item() <= 1e-5
     for got, t in zip(grads, (q, k, v, table)):
         assert (got - t.grad).abs().max().item() <= 1e-4 * max(1.0, t.grad.abs().max().item())
+
+
+def test_tc_kernel_selected_for_swin_shapes():
+    for d in (16, 32, 64):
+        for dt in (torch.float16, torch.bfloat16):
+            assert ops.footprint(8192, 3, 49, d, dt)["kernel_fwd"] == "tc"
+            assert ops.footprint(100, 2, 64, d, dt)["kernel_fwd"] == "tc"
+    assert ops.footprint(64, 3, 49, 32, torch.float32)["kernel_fwd"] == "generic"
+    assert ops.footprint(64, 3, 49, 10, torch.float16)["kernel_fwd"] == "generic"
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("units", [1, 2, 3, 295, 296, 297, 593, 4097])
+def test_tc_forward_tile_counts(dt, units):
+    """Odd unit counts (half-empty last tile) and grid wrap-around of the persistent scheduler."""
+    dtype = DTYPES[dt]
+    (q, k, v), (qh, kh, vh) = draw(units, (units, 1, 49, 32), 3, dtype)
+    o = ops.attention_forward(q, k, v, 0.2, kernel="tc")
+    ref, _ = orc.attention_forward(qh, kh, vh, 0.2)
+    ok, err = err_ok(o, ref, dtype)
+    assert ok, err
+
+
+def test_tc_forward_does_not_write_outside_output():
+    """Rows L..63 of the padded tile and the phantom unit of the last tile are clipped by TMA."""
+    q, k, v = (fwa.fill_uniform(fwa.Rng(i), (3, 1, 49, 32), dtype=torch.float16) for i in range(3))
+    big = torch.full((4 * 49 * 32 + 4096,), 7.0, dtype=torch.float16, device="cuda")
+    out = big[: 3 * 49 * 32].view(3, 1, 49, 32)
+    ops.attention_forward(q, k, v, 0.2, kernel="tc", out=out)
+    torch.cuda.synchronize()
+    assert (big[3 * 49 * 32:] == 7.0).all()
 
 
 def test_footprint_reports_kernel_and_paper_peaks():
