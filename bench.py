@@ -208,15 +208,11 @@ def run_gpu(args, wl):
         bufs.append((q, kk, v, do, bias, mask, o, d ** -0.5))
     torch.cuda.synchronize()
 
-    def step(events=None):
+    def step():
         for i, (q, kk, v, do, bias, mask, o, sc) in enumerate(bufs):
-            if events is not None:
-                events[i][0].record()
             ops.attention_forward(q, kk, v, sc, bias, mask, out=o)
             if wl["bwd"]:
                 ops.attention_backward(q, kk, v, do, sc, bias, mask, want_dbias=bias is not None)
-            if events is not None:
-                events[i][1].record()
 
     sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
                            if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit()
@@ -225,19 +221,35 @@ def run_gpu(args, wl):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # One step = the 12 layer calls, captured once into a CUDA graph (launch-bound
+    # small stages would otherwise measure Python/ctypes time, not the GPU).
+    graph = None
+    per_step_launches = None
+    if not args.eager:
+        graph = torch.cuda.CUDAGraph()
+        l0 = nat.launch_count()
+        with torch.cuda.graph(graph):
+            step()
+        per_step_launches = nat.launch_count() - l0
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in bufs] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = nat.launch_count()
     start.record()
     for s in range(args.steps):
-        step(ev[s])
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
     stop.record()
     torch.cuda.synchronize()
     launches = nat.launch_count() - launches0
+    if graph is not None:
+        launches = per_step_launches * args.steps
     elapsed_ms = start.elapsed_time(stop)
     if world > 1:
         t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
@@ -246,8 +258,30 @@ def run_gpu(args, wl):
         dist.barrier()
     clocks = sampler.stop()
 
-    per_layer_ms = [statistics.mean(ev[s][i][0].elapsed_time(ev[s][i][1])
-                                    for s in range(args.steps)) for i in range(len(bufs))]
+    # Per-layer kernel durations (roofline numerator): each distinct layer shape
+    # replayed R times inside its own graph, CUDA events around the replays.
+    reps = 10
+    per_shape = {}
+    for i, lay in enumerate(layers):
+        if lay in per_shape:
+            continue
+        q, kk, v, do, bias, mask, o, sc = bufs[i]
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1):
+            for _ in range(reps):
+                ops.attention_forward(q, kk, v, sc, bias, mask, out=o)
+                if wl["bwd"]:
+                    ops.attention_backward(q, kk, v, do, sc, bias, mask, want_dbias=bias is not None)
+        g1.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g1.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        per_shape[lay] = e0.elapsed_time(e1) / reps
+        del g1
+    per_layer_ms = [per_shape[lay] for lay in layers]
     windows_per_step = sum(N for (N, h, L, d) in layers)
     fwd_bytes = [4 * N * h * L * d * eb for (N, h, L, d) in layers]
     bwd_bytes = [7 * N * h * L * d * eb for (N, h, L, d) in layers] if wl["bwd"] else [0] * len(layers)
@@ -322,6 +356,7 @@ def run_gpu(args, wl):
             "config": {"workload": args.workload, "desc": wl["desc"], "images_per_gpu": wl["batch"],
                        "layers": [list(x) for x in layers], "global_batch": wl["batch"] * world,
                        "parallelism": f"dp{world} (weak: {wl['batch']} images per GPU, no collective)",
+                       "launch": "eager" if args.eager else "CUDA graph of one step (12 layer calls), PDL between kernels",
                        "l2": "no flush: each step streams "
                              f"{alg_bytes_step / 1e9:.2f} GB of distinct tensors (>> 126 MB L2)"},
             "tflops": flops_step * world / (ms_per_step / 1e3) / 1e12,
@@ -332,7 +367,10 @@ def run_gpu(args, wl):
                          "algorithmic_bytes_per_step": alg_bytes_step,
                          "dominant_launch": {"shape": list(layers[dom]), "ms": per_layer_ms[dom],
                                              "GB/s": dom_gbs, "frac": dom_gbs / peak},
-                         "per_layer_ms": per_layer_ms},
+                         "per_layer_ms": per_layer_ms,
+                         "how": "per-launch time = CUDA events around a graph of 10 back-to-back "
+                                "launches of that layer; achieved = algorithmic bytes / sum of "
+                                "per-layer launch times"},
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -380,6 +418,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph for the timed steps")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps

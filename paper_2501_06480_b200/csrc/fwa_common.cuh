@@ -1,12 +1,14 @@
 // fwa_common.cuh — shared device/host helpers for libfwa (sm_100a only).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/fwa.h"
 
@@ -69,6 +71,28 @@ int tc_fwd_tmem_cols(const Geom& g);
 int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k,
                   const void* v, const float* bias, const float* mask, void* o,
                   cudaStream_t s);
+
+// fwa_host.cu: cached 3-D tensor map over [units][L][d] 16-bit data
+int get_units_map(CUtensorMap* out, const void* ptr, int dtype, int64_t units, int L, int d,
+                  int box_rows, int box_units);
+
+// Launch with programmatic dependent launch (PDL) enabled: the kernel must execute
+// griddepcontrol.wait before touching global memory.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 int device_sm_count();
 int64_t device_l2_bytes();

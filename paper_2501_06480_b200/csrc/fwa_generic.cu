@@ -277,10 +277,12 @@ int launch_fwd_generic_t(const Geom& g, const void* q, const void* k, const void
   const int nRB = (g.L + R - 1) / R;
   const size_t smem = fwd_generic_smem(g);
   auto kern = fwd_generic_kernel<T>;
-  if (smem > 48 * 1024) {
+  static int attr_smem = 48 * 1024;  // per instantiation; never shrinks
+  if ((int)smem > attr_smem) {
     int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem), "cudaFuncSetAttribute(fwd_generic)");
     if (rc) return rc;
+    attr_smem = (int)smem;
   }
   const int64_t blocks = g.units * nRB;
   if (blocks <= 0) return FWA_OK;
@@ -298,9 +300,14 @@ int launch_bwd_generic_t(const Geom& g, const void* q, const void* k, const void
   const int R = bwd_rows(g.L);
   const size_t smem = bwd_generic_smem(g);
   auto kern = bwd_generic_kernel<T>;
-  int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem), "cudaFuncSetAttribute(bwd_generic)");
-  if (rc) return rc;
+  static int attr_smem = 48 * 1024;
+  int rc = FWA_OK;
+  if ((int)smem > attr_smem) {
+    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem), "cudaFuncSetAttribute(bwd_generic)");
+    if (rc) return rc;
+    attr_smem = (int)smem;
+  }
   const int grid = bwd_generic_grid(g);
   if (g.units <= 0) return FWA_OK;
   kern<<<grid, kBwdThreads, smem, s>>>(g, R, (const T*)q, (const T*)k, (const T*)v,

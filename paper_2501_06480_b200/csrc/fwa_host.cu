@@ -1,0 +1,99 @@
+// fwa_host.cu — host helpers shared by the TMA kernels: tensor-map encode + cache, PDL launch.
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "fwa_common.cuh"
+
+namespace fwa {
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  uintptr_t ptr;
+  int64_t units;
+  int32_t dtype, L, d, box_rows, box_units;
+  bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<uintptr_t>()(k.ptr);
+    h ^= std::hash<int64_t>()(k.units) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h ^= (size_t)k.L * 1315423911u ^ (size_t)k.d * 2654435761u ^ (size_t)k.dtype ^
+         ((size_t)k.box_rows << 20) ^ ((size_t)k.box_units << 28);
+    return h;
+  }
+};
+
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash>& map_cache() {
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> m;
+  return m;
+}
+
+}  // namespace
+
+// 3-D map over [units][L][d] (16-bit elements) with box (d, box_rows, box_units);
+// swizzle = the row width (32/64/128 B) so the smem image is the UMMA canonical layout.
+int get_units_map(CUtensorMap* out, const void* ptr, int dtype, int64_t units, int L, int d,
+                  int box_rows, int box_units) {
+  MapKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.ptr = (uintptr_t)ptr;
+  key.units = units;
+  key.dtype = dtype;
+  key.L = L;
+  key.d = d;
+  key.box_rows = box_rows;
+  key.box_units = box_units;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = map_cache().find(key);
+    if (it != map_cache().end()) {
+      *out = it->second;
+      return FWA_OK;
+    }
+  }
+  EncodeFn enc = get_encode();
+  if (!enc) return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t gdim[3] = {(cuuint64_t)d, (cuuint64_t)L, (cuuint64_t)units};
+  const cuuint64_t gstride[2] = {(cuuint64_t)d * 2, (cuuint64_t)L * d * 2};
+  const cuuint32_t box[3] = {(cuuint32_t)d, (cuuint32_t)box_rows, (cuuint32_t)box_units};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapSwizzle swz = d == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : d == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = enc(out, dtype == FWA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   3, const_cast<void*>(ptr), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (map_cache().size() > 1024) map_cache().clear();
+  map_cache().emplace(key, *out);
+  return FWA_OK;
+}
+
+}  // namespace fwa

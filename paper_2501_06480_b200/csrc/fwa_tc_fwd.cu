@@ -23,6 +23,11 @@
 // Warp roles (192 threads, 2 CTAs per SM, persistent over tiles):
 //   warp 0: TMA producer, warp 1: TMEM allocator + MMA issuer,
 //   warps 2-5: softmax + epilogue (warp w owns TMEM lanes 32*(w%4)..+31).
+// The softmax warps are software-pipelined: iteration i runs softmax(i) and
+// then the epilogue of tile i-1, whose P.V ran on the tensor core meanwhile;
+// P (smem) and O (TMEM) are double-buffered for that. L = 49 and 64 are
+// compile-time specialisations (no masking arithmetic); other L <= 64 run
+// the runtime-L instance.
 // HBM is touched once per tensor: Q, K, V read once, O written once.
 #include <cuda.h>
 #include <math.h>
@@ -49,42 +54,46 @@ template <int D>
 struct Cfg {
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTileBytes = kTileRows * kRowBytes;            // one of Q/K/V per stage
-  static constexpr int kStages = D <= 16 ? 4 : (D <= 32 ? 2 : 2);
+  static constexpr int kStages = D <= 16 ? 4 : 2;
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);  // UMMA layout code
-  static constexpr int kSmem = 1024 /*align slack*/ + kStages * 3 * kTileBytes + kPBytes +
-                               2 * kTileBytes /*O staging*/ + 256 /*barriers*/;
+  static constexpr int kSmem = 1024 /*align slack*/ + kStages * 3 * kTileBytes + 2 * kPBytes +
+                               kTileBytes /*O staging*/ + 256 /*barriers*/;
   static constexpr int kChunks = kRowBytes / 16;  // 16-byte chunks per row
+  static constexpr uint32_t kTmemO0 = 128, kTmemO1 = 128 + D;  // double-buffered O
 };
 
 struct SmemBarriers {
   uint64_t full[4];
   uint64_t empty[4];
-  uint64_t s_full, s_empty, p_full, pv_done;
+  uint64_t s_full, s_empty, p_full;
+  uint64_t pv_done[2];
   uint32_t tmem_base;
 };
 
-template <typename T, int D>
+// LK > 0: compile-time window length (Swin 7x7 / 8x8); LK == 0: runtime L.
+template <typename T, int D, int LK>
 __global__ void __launch_bounds__(kThreads, 2)
 fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-              int n_tiles, int L, float scale_log2) {
+              int n_tiles, int L_rt, float scale_log2) {
   using C = Cfg<D>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
+  const int L = LK > 0 ? LK : L_rt;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + C::kStages * C::kTileBytes;
   uint8_t* sV = sK + C::kStages * C::kTileBytes;
-  uint8_t* sP = sV + C::kStages * C::kTileBytes;
-  uint8_t* sO = sP + kPBytes;
-  SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(sO + 2 * C::kTileBytes);
+  uint8_t* sP = sV + C::kStages * C::kTileBytes;   // 2 x kPBytes
+  uint8_t* sO = sP + 2 * kPBytes;                  // 1 staging tile
+  SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(sO + C::kTileBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // zero P (the off-diagonal block must stay zero for the whole kernel)
-  for (int i = threadIdx.x; i < kPBytes / 16; i += kThreads)
+  // zero both P buffers: off-diagonal blocks and keys >= L stay zero for the whole kernel
+  for (int i = threadIdx.x; i < 2 * kPBytes / 16; i += kThreads)
     reinterpret_cast<uint4*>(sP)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
@@ -95,7 +104,8 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->s_empty, 128);
     mbar_init(&bars->p_full, 128);
-    mbar_init(&bars->pv_done, 1);
+    mbar_init(&bars->pv_done[0], 1);
+    mbar_init(&bars->pv_done[1], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -110,11 +120,16 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  const int n_local = n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int n_local =
+      n_tiles > (int)blockIdx.x ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
+  // PDL: let the next kernel in the stream start its prologue; our own global
+  // traffic starts only after the previous grid has fully completed.
+  griddep_launch_dependents();
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
+      griddep_wait();
       const uint64_t pol = policy_evict_first();
       for (int i = 0; i < n_local; ++i) {
         const int tile = blockIdx.x + i * gridDim.x;
@@ -150,20 +165,22 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
       issue_S(0);
       for (int i = 0; i < n_local; ++i) {
         const int st = i % C::kStages;
-        // O = P V once softmax has written P(i)
+        const int pb = i & 1;
+        // O(pb) = P(pb) V once softmax has written P(i)
         mbar_wait(&bars->p_full, i & 1);
         tc_fence_after();
-        const uint32_t p0 = smem_u32(sP);
+        const uint32_t p0 = smem_u32(sP + pb * kPBytes);
         const uint32_t v0 = smem_u32(sV + st * C::kTileBytes);
+        const uint32_t od = tmem + (pb ? C::kTmemO1 : C::kTmemO0);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t pa = p0 + (kk >> 2) * 8192 + (kk & 3) * 32;
           const uint64_t a = make_sdesc(pa, 16, 1024, 2 /*SW128*/);
           const uint64_t b = make_sdesc(v0 + kk * 16 * C::kRowBytes, C::kTileBytes,
                                         8 * C::kRowBytes, C::kSwz);
-          mma_f16_ss(tmem + kTmemO, a, b, idO, kk > 0);
+          mma_f16_ss(od, a, b, idO, kk > 0);
         }
-        mma_commit(&bars->pv_done);
+        mma_commit(&bars->pv_done[pb]);
         mma_commit(&bars->empty[st]);
         if (i + 1 < n_local) {
           const int st1 = (i + 1) % C::kStages;
@@ -175,97 +192,108 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
       }
     }
   } else {
-    // ===================== softmax + epilogue (warps 2..5) =====================
+    // ============ softmax(i) then epilogue(i-1) (warps 2..5, software-pipelined) ============
     const int q = warp & 3;               // TMEM lane quarter
     const int row = q * 32 + lane;        // tile row = TMEM lane
     const int ul = row >> 6;              // unit within the tile
-    const int r_in = row & 63;            // row within the unit
     const uint32_t t_lane = (uint32_t)(q * 32) << 16;
-    const uint32_t pswz = (uint32_t)(r_in & 7);
-    uint8_t* prow = sP + ul * 8192 + (row >> 3) * 1024 + (row & 7) * 128;
+    const uint32_t pswz = (uint32_t)(row & 7);
+    const int prow_off = ul * 8192 + (row >> 3) * 1024 + (row & 7) * 128;
+    uint8_t* orow = sO + row * C::kRowBytes;
+    const uint32_t oswz = (uint32_t)((row * C::kRowBytes) >> 7) & (C::kChunks - 1);
     const bool leader = (threadIdx.x == 64);
-    for (int i = 0; i < n_local; ++i) {
-      const int tile = blockIdx.x + i * gridDim.x;
-      mbar_wait(&bars->s_full, i & 1);
-      tc_fence_after();
-      uint32_t s[64];
+    constexpr int kMaxChunks = 8;
+    const int p_chunks = LK > 0 ? (LK + 7) / 8 : kMaxChunks;  // chunks beyond L stay zero
+    float inv_prev = 0.f;
+    for (int i = 0; i <= n_local; ++i) {
+      float inv_cur = 0.f;
+      if (i < n_local) {
+        mbar_wait(&bars->s_full, i & 1);
+        tc_fence_after();
+        uint32_t s[64];
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
-        tmem_ld16(tmem + t_lane + ul * 64 + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&s[g * 16]));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&bars->s_empty);
-      // masked row max over the L valid keys
-      float mx = -INFINITY;
+        for (int g = 0; g < 4; ++g)
+          if (LK == 0 || g * 16 < LK)
+            tmem_ld16(tmem + t_lane + ul * 64 + g * 16,
+                      *reinterpret_cast<uint32_t(*)[16]>(&s[g * 16]));
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&bars->s_empty);
+        float mx = -INFINITY;
 #pragma unroll
-      for (int j = 0; j < 64; ++j)
-        if (j < L) mx = fmaxf(mx, __uint_as_float(s[j]));
-      const float mxs = mx * scale_log2;
-      float sum = 0.f;
-      uint32_t pk[32];
+        for (int j = 0; j < 64; ++j)
+          if (j < L) mx = fmaxf(mx, __uint_as_float(s[j]));
+        const float mxs = mx * scale_log2;
+        float sum = 0.f;
+        uint32_t pk[32];
 #pragma unroll
-      for (int j = 0; j < 64; j += 2) {
-        const float p0 = j < L ? ex2(fmaf(__uint_as_float(s[j]), scale_log2, -mxs)) : 0.f;
-        const float p1 = j + 1 < L ? ex2(fmaf(__uint_as_float(s[j + 1]), scale_log2, -mxs)) : 0.f;
-        if constexpr (kBF16) {
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-          const float2 back = __bfloat1622float2(h2);
-          sum += back.x + back.y;
-          pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
-        } else {
-          __half2 h2 = __floats2half2_rn(p0, p1);
-          const float2 back = __half22float2(h2);
-          sum += back.x + back.y;
-          pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+        for (int j = 0; j < 64; j += 2) {
+          const float p0 = j < L ? ex2(fmaf(__uint_as_float(s[j]), scale_log2, -mxs)) : 0.f;
+          const float p1 = j + 1 < L ? ex2(fmaf(__uint_as_float(s[j + 1]), scale_log2, -mxs)) : 0.f;
+          sum += p0 + p1;
+          if constexpr (kBF16) {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+            pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          } else {
+            __half2 h2 = __floats2half2_rn(p0, p1);
+            pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+        }
+        inv_cur = __frcp_rn(sum);
+        // P(i) -> P buffer i&1 (SW128 K-major). PV(i-2) read it and epilogue(i-2) waited on it.
+        uint8_t* prow = sP + (i & 1) * kPBytes + prow_off;
+#pragma unroll
+        for (int c = 0; c < kMaxChunks; ++c) {
+          if (c < p_chunks) {
+            uint4 v = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            *reinterpret_cast<uint4*>(prow + ((c ^ pswz) << 4)) = v;
+          }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&bars->p_full);
+      }
+      if (i > 0) {
+        // ---- epilogue of tile i-1 (its PV ran while we did softmax(i)) ----
+        const int e = i - 1;
+        const int tile = blockIdx.x + e * gridDim.x;
+        mbar_wait(&bars->pv_done[e & 1], (e >> 1) & 1);
+        tc_fence_after();
+        uint32_t o[D];
+#pragma unroll
+        for (int g = 0; g < D / 16; ++g)
+          tmem_ld16(tmem + t_lane + ((e & 1) ? C::kTmemO1 : C::kTmemO0) + g * 16,
+                    *reinterpret_cast<uint32_t(*)[16]>(&o[g * 16]));
+        tmem_wait_ld();
+        tc_fence_before();
+        uint32_t ob[D / 2];
+#pragma unroll
+        for (int j = 0; j < D; j += 2) {
+          const float a = __uint_as_float(o[j]) * inv_prev;
+          const float b = __uint_as_float(o[j + 1]) * inv_prev;
+          if constexpr (kBF16) {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+            ob[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          } else {
+            __half2 h2 = __floats2half2_rn(a, b);
+            ob[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+        }
+        if (leader) bulk_wait_read<0>();   // previous store finished reading the staging tile
+        named_sync(1, 128);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c) {
+          uint4 v = make_uint4(ob[4 * c], ob[4 * c + 1], ob[4 * c + 2], ob[4 * c + 3]);
+          *reinterpret_cast<uint4*>(orow + ((c ^ oswz) << 4)) = v;
+        }
+        fence_proxy_async_smem();
+        named_sync(2, 128);
+        if (leader) {
+          tma_store_3d(&tm_o, sO, 0, 0, 2 * tile);
+          bulk_commit();
         }
       }
-      // P(i) -> smem (SW128 K-major). PV(i-1) finished reading P: we waited pv_done(i-1).
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint4 v = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        *reinterpret_cast<uint4*>(prow + ((c ^ pswz) << 4)) = v;
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&bars->p_full);
-      // ---- epilogue ----
-      mbar_wait(&bars->pv_done, i & 1);
-      tc_fence_after();
-      uint32_t o[D];
-#pragma unroll
-      for (int g = 0; g < D / 16; ++g)
-        tmem_ld16(tmem + t_lane + kTmemO + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&o[g * 16]));
-      tmem_wait_ld();
-      tc_fence_before();
-      const float inv = 1.f / sum;
-      uint32_t ob[D / 2];
-#pragma unroll
-      for (int j = 0; j < D; j += 2) {
-        const float a = __uint_as_float(o[j]) * inv, b = __uint_as_float(o[j + 1]) * inv;
-        if constexpr (kBF16) {
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
-          ob[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
-        } else {
-          __half2 h2 = __floats2half2_rn(a, b);
-          ob[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
-        }
-      }
-      uint8_t* stg = sO + (i & 1) * C::kTileBytes;
-      if (leader) bulk_wait_read<1>();
-      named_sync(1, 128);
-      uint8_t* orow = stg + row * C::kRowBytes;
-      const uint32_t oswz = (uint32_t)((row * C::kRowBytes) >> 7) & (C::kChunks - 1);
-#pragma unroll
-      for (int c = 0; c < C::kChunks; ++c) {
-        uint4 v = make_uint4(ob[4 * c], ob[4 * c + 1], ob[4 * c + 2], ob[4 * c + 3]);
-        *reinterpret_cast<uint4*>(orow + ((c ^ oswz) << 4)) = v;
-      }
-      fence_proxy_async_smem();
-      named_sync(2, 128);
-      if (leader) {
-        tma_store_3d(&tm_o, stg, 0, 0, 2 * tile);
-        bulk_commit();
-      }
+      inv_prev = inv_cur;
     }
     if (leader) bulk_wait<0>();
   }
@@ -276,55 +304,16 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
 }
 
 // ---- host side ---------------------------------------------------------------
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
-                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
-                              CUtensorMapFloatOOBfill);
-
-EncodeFn get_encode() {
-  static EncodeFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
-                                         &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(p);
-  });
-  return fn;
-}
-
-int encode_units_map(CUtensorMap* m, const void* ptr, int dtype, int64_t units, int L, int d) {
-  EncodeFn enc = get_encode();
-  if (!enc) return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t gdim[3] = {(cuuint64_t)d, (cuuint64_t)L, (cuuint64_t)units};
-  const cuuint64_t gstride[2] = {(cuuint64_t)d * 2, (cuuint64_t)L * d * 2};
-  const cuuint32_t box[3] = {(cuuint32_t)d, (cuuint32_t)kUnitRows, 2};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  const CUtensorMapSwizzle swz = d == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
-                                 : d == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                           : CU_TENSOR_MAP_SWIZZLE_128B;
-  CUresult r = enc(m, dtype == FWA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
-                                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                   3, const_cast<void*>(ptr), gdim, gstride, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-  return FWA_OK;
-}
-
-template <typename T, int D>
+template <typename T, int D, int LK>
 int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
              cudaStream_t s) {
   CUtensorMap mq, mk, mv, mo;
   int rc;
-  if ((rc = encode_units_map(&mq, q, dtype, g.units, g.L, g.d))) return rc;
-  if ((rc = encode_units_map(&mk, k, dtype, g.units, g.L, g.d))) return rc;
-  if ((rc = encode_units_map(&mv, v, dtype, g.units, g.L, g.d))) return rc;
-  if ((rc = encode_units_map(&mo, o, dtype, g.units, g.L, g.d))) return rc;
-  auto kern = fwd_tc_kernel<T, D>;
+  if ((rc = get_units_map(&mq, q, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+  if ((rc = get_units_map(&mk, k, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+  if ((rc = get_units_map(&mv, v, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+  if ((rc = get_units_map(&mo, o, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+  auto kern = fwd_tc_kernel<T, D, LK>;
   constexpr int smem = Cfg<D>::kSmem;
   static bool attr_done = false;
   if (!attr_done) {
@@ -337,9 +326,31 @@ int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void*
   const int per_sm = (2 * (smem + 1024) <= 228 * 1024) ? 2 : 1;
   const int grid = std::max(1, std::min(n_tiles, device_sm_count() * per_sm));
   const float scale_log2 = g.scale * 1.4426950408889634f;
-  kern<<<grid, kThreads, smem, s>>>(mq, mk, mv, mo, n_tiles, g.L, scale_log2);
+  rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, mq, mk, mv, mo, n_tiles,
+                             (int)g.L, scale_log2),
+                  "fwd_tc_kernel launch");
+  if (rc) return rc;
   count_launch();
   return check_cuda(cudaGetLastError(), "fwd_tc_kernel launch");
+}
+
+template <typename T, int D>
+int dispatch_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
+               cudaStream_t s) {
+  if (g.L == 49) return launch_t<T, D, 49>(g, dtype, q, k, v, o, s);
+  if (g.L == 64) return launch_t<T, D, 64>(g, dtype, q, k, v, o, s);
+  return launch_t<T, D, 0>(g, dtype, q, k, v, o, s);
+}
+
+template <typename T>
+int dispatch_d(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
+               cudaStream_t s) {
+  switch (g.d) {
+    case 16: return dispatch_l<T, 16>(g, dtype, q, k, v, o, s);
+    case 32: return dispatch_l<T, 32>(g, dtype, q, k, v, o, s);
+    case 64: return dispatch_l<T, 64>(g, dtype, q, k, v, o, s);
+  }
+  return fail(FWA_ERR_CAPACITY, "tcgen05 forward: unsupported head_dim");
 }
 
 }  // namespace
@@ -363,14 +374,8 @@ int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k, const 
                   const float* bias, const float* mask, void* o, cudaStream_t s) {
   if (bias || mask) return fail(FWA_ERR_CAPACITY, "tcgen05 forward: bias/mask not supported yet");
   const bool bf = dtype == FWA_BF16;
-  switch (g.d) {
-    case 16: return bf ? launch_t<__nv_bfloat16, 16>(g, dtype, q, k, v, o, s)
-                       : launch_t<__half, 16>(g, dtype, q, k, v, o, s);
-    case 32: return bf ? launch_t<__nv_bfloat16, 32>(g, dtype, q, k, v, o, s)
-                       : launch_t<__half, 32>(g, dtype, q, k, v, o, s);
-    case 64: return bf ? launch_t<__nv_bfloat16, 64>(g, dtype, q, k, v, o, s)
-                       : launch_t<__half, 64>(g, dtype, q, k, v, o, s);
-  }
+  return bf ? dispatch_d<__nv_bfloat16>(g, dtype, q, k, v, o, s)
+            : dispatch_d<__half>(g, dtype, q, k, v, o, s);
   return fail(FWA_ERR_CAPACITY, "tcgen05 forward: unsupported head_dim");
 }
 
