@@ -13,10 +13,13 @@
 //     [0,128). Only the two diagonal 64x64 blocks are used.
 //   * Softmax: 4 warps, one thread per row (TMEM lane = row): tcgen05.ld of the
 //     row's own 64-column block, masked max over the L valid keys, ex2, row
-//     sum; P (unnormalised, f16/bf16) goes to shared memory in the SW128
-//     K-major layout. The two off-diagonal 64x64 blocks of P share one zeroed
-//     8 KB region (24 KB instead of 32 KB).
-//   * O = P V: tcgen05.mma (M=128, N=d, K=128) into TMEM columns [128,128+d).
+//     sum; P (unnormalised, f16/bf16 pairs) is written back to TMEM with
+//     tcgen05.st (columns [128,192); the other unit's half of each row stays
+//     zero), so P never touches shared memory.
+//   * O = P V: tcgen05.mma with A from TMEM (M=128, N=d, K=128) into TMEM
+//     (double-buffered O at [192, 192+2d)).
+//   * Shared memory holds only the TMA ring (4 stages for d=32, 8 for d=16)
+//     and one staging tile for the TMA store.
 //   * Epilogue: tcgen05.ld, scale by 1/rowsum, convert, swizzled staging,
 //     TMA store with the same 3-D map (rows >= L are clipped by the map).
 //
@@ -46,25 +49,25 @@ using namespace sm100;
 constexpr int kThreads = 192;
 constexpr int kTileRows = 128;     // MMA M
 constexpr int kUnitRows = 64;      // rows per packed unit
-constexpr int kPBytes = 24 * 1024; // P tile with the shared zero block
-constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kTmemO = 128;   // O accumulator column offset
 
 template <int D>
 struct Cfg {
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTileBytes = kTileRows * kRowBytes;            // one of Q/K/V per stage
-  static constexpr int kStages = D <= 16 ? 4 : 2;
+  static constexpr int kStages = D <= 16 ? 8 : 4;
+  static constexpr int kCtasPerSm = D <= 32 ? 2 : 1;
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);  // UMMA layout code
-  static constexpr int kSmem = 1024 /*align slack*/ + kStages * 3 * kTileBytes + 2 * kPBytes +
+  static constexpr int kSmem = 1024 /*align slack*/ + kStages * 3 * kTileBytes +
                                kTileBytes /*O staging*/ + 256 /*barriers*/;
   static constexpr int kChunks = kRowBytes / 16;  // 16-byte chunks per row
-  static constexpr uint32_t kTmemO0 = 128, kTmemO1 = 128 + D;  // double-buffered O
+  // TMEM columns: S [0,128) fp32 | P [128,192) 16-bit pairs | O0, O1 (d each) fp32
+  static constexpr uint32_t kTmemP = 128, kTmemO0 = 192, kTmemO1 = 192 + D;
+  static constexpr uint32_t kTmemCols = 192 + 2 * D <= 256 ? 256 : 512;
 };
 
 struct SmemBarriers {
-  uint64_t full[4];
-  uint64_t empty[4];
+  uint64_t full[8];
+  uint64_t empty[8];
   uint64_t s_full, s_empty, p_full;
   uint64_t pv_done[2];
   uint32_t tmem_base;
@@ -72,7 +75,7 @@ struct SmemBarriers {
 
 // LK > 0: compile-time window length (Swin 7x7 / 8x8); LK == 0: runtime L.
 template <typename T, int D, int LK>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, Cfg<D>::kCtasPerSm)
 fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
               int n_tiles, int L_rt, float scale_log2) {
@@ -85,17 +88,12 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + C::kStages * C::kTileBytes;
   uint8_t* sV = sK + C::kStages * C::kTileBytes;
-  uint8_t* sP = sV + C::kStages * C::kTileBytes;   // 2 x kPBytes
-  uint8_t* sO = sP + 2 * kPBytes;                  // 1 staging tile
+  uint8_t* sO = sV + C::kStages * C::kTileBytes;   // 1 staging tile for the TMA store
   SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(sO + C::kTileBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // zero both P buffers: off-diagonal blocks and keys >= L stay zero for the whole kernel
-  for (int i = threadIdx.x; i < 2 * kPBytes / 16; i += kThreads)
-    reinterpret_cast<uint4*>(sP)[i] = make_uint4(0, 0, 0, 0);
-  fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&bars->full[s], 1);
@@ -114,7 +112,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
     tma_prefetch_desc(&tm_v);
     tma_prefetch_desc(&tm_o);
   }
-  if (warp == 1) tmem_alloc(&bars->tmem_base, kTmemCols);
+  if (warp == 1) tmem_alloc(&bars->tmem_base, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -164,24 +162,8 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
       tc_fence_after();
       issue_S(0);
       for (int i = 0; i < n_local; ++i) {
-        const int st = i % C::kStages;
-        const int pb = i & 1;
-        // O(pb) = P(pb) V once softmax has written P(i)
-        mbar_wait(&bars->p_full, i & 1);
-        tc_fence_after();
-        const uint32_t p0 = smem_u32(sP + pb * kPBytes);
-        const uint32_t v0 = smem_u32(sV + st * C::kTileBytes);
-        const uint32_t od = tmem + (pb ? C::kTmemO1 : C::kTmemO0);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t pa = p0 + (kk >> 2) * 8192 + (kk & 3) * 32;
-          const uint64_t a = make_sdesc(pa, 16, 1024, 2 /*SW128*/);
-          const uint64_t b = make_sdesc(v0 + kk * 16 * C::kRowBytes, C::kTileBytes,
-                                        8 * C::kRowBytes, C::kSwz);
-          mma_f16_ss(od, a, b, idO, kk > 0);
-        }
-        mma_commit(&bars->pv_done[pb]);
-        mma_commit(&bars->empty[st]);
+        // S(i+1) as soon as softmax(i) has pulled S(i) into registers: it runs on the
+        // tensor core while softmax(i) computes.
         if (i + 1 < n_local) {
           const int st1 = (i + 1) % C::kStages;
           mbar_wait(&bars->full[st1], ((i + 1) / C::kStages) & 1);
@@ -189,6 +171,21 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
           tc_fence_after();
           issue_S(i + 1);
         }
+        const int st = i % C::kStages;
+        const int ob = i & 1;
+        // O(ob) = P V, P read from TMEM (TS form), once softmax has stored P(i)
+        mbar_wait(&bars->p_full, i & 1);
+        tc_fence_after();
+        const uint32_t v0 = smem_u32(sV + st * C::kTileBytes);
+        const uint32_t od = tmem + (ob ? C::kTmemO1 : C::kTmemO0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t b = make_sdesc(v0 + kk * 16 * C::kRowBytes, C::kTileBytes,
+                                        8 * C::kRowBytes, C::kSwz);
+          mma_f16_ts(od, tmem + C::kTmemP + kk * 8, b, idO, kk > 0);
+        }
+        mma_commit(&bars->pv_done[ob]);
+        mma_commit(&bars->empty[st]);
       }
     }
   } else {
@@ -197,13 +194,17 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
     const int row = q * 32 + lane;        // tile row = TMEM lane
     const int ul = row >> 6;              // unit within the tile
     const uint32_t t_lane = (uint32_t)(q * 32) << 16;
-    const uint32_t pswz = (uint32_t)(row & 7);
-    const int prow_off = ul * 8192 + (row >> 3) * 1024 + (row & 7) * 128;
     uint8_t* orow = sO + row * C::kRowBytes;
     const uint32_t oswz = (uint32_t)((row * C::kRowBytes) >> 7) & (C::kChunks - 1);
     const bool leader = (threadIdx.x == 64);
-    constexpr int kMaxChunks = 8;
-    const int p_chunks = LK > 0 ? (LK + 7) / 8 : kMaxChunks;  // chunks beyond L stay zero
+    // the other unit's 32 P columns of this row stay zero for the whole kernel
+    {
+      uint32_t z[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) z[j] = 0u;
+      tmem_st32(tmem + t_lane + C::kTmemP + (1 - ul) * 32, z);
+      tmem_wait_st();
+    }
     float inv_prev = 0.f;
     for (int i = 0; i <= n_local; ++i) {
       float inv_cur = 0.f;
@@ -240,16 +241,13 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
           }
         }
         inv_cur = __frcp_rn(sum);
-        // P(i) -> P buffer i&1 (SW128 K-major). PV(i-2) read it and epilogue(i-2) waited on it.
-        uint8_t* prow = sP + (i & 1) * kPBytes + prow_off;
-#pragma unroll
-        for (int c = 0; c < kMaxChunks; ++c) {
-          if (c < p_chunks) {
-            uint4 v = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-            *reinterpret_cast<uint4*>(prow + ((c ^ pswz) << 4)) = v;
-          }
+        // P(i) -> TMEM (own unit's 32 columns) once PV(i-1) has consumed P(i-1)
+        if (i > 0) {
+          mbar_wait(&bars->pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
+          tc_fence_after();
         }
-        fence_proxy_async_smem();
+        tmem_st32(tmem + t_lane + C::kTmemP + ul * 32, pk);
+        tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->p_full);
       }
@@ -300,7 +298,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, kTmemCols);
+  if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -323,7 +321,7 @@ int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void*
     attr_done = true;
   }
   const int n_tiles = (int)((g.units + 1) / 2);
-  const int per_sm = (2 * (smem + 1024) <= 228 * 1024) ? 2 : 1;
+  const int per_sm = Cfg<D>::kCtasPerSm;
   const int grid = std::max(1, std::min(n_tiles, device_sm_count() * per_sm));
   const float scale_log2 = g.scale * 1.4426950408889634f;
   rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, mq, mk, mv, mo, n_tiles,
@@ -368,7 +366,9 @@ size_t tc_fwd_smem(const Geom& g, int) {
   return g.d == 16 ? Cfg<16>::kSmem : g.d == 32 ? Cfg<32>::kSmem : Cfg<64>::kSmem;
 }
 
-int tc_fwd_tmem_cols(const Geom&) { return (int)kTmemCols; }
+int tc_fwd_tmem_cols(const Geom& g) {
+  return g.d == 16 ? Cfg<16>::kTmemCols : g.d == 32 ? Cfg<32>::kTmemCols : Cfg<64>::kTmemCols;
+}
 
 int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                   const float* bias, const float* mask, void* o, cudaStream_t s) {
