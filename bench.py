@@ -234,6 +234,12 @@ def run_gpu(args, wl):
         for _ in range(3):
             graph.replay()
         torch.cuda.synchronize()
+    # clock soak: keep the GPU busy ~1.5 s so nvidia-smi samples the loaded clocks
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < args.soak_s:
+        for _ in range(20):
+            graph.replay() if graph is not None else step()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -419,6 +425,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the timed steps")
+    ap.add_argument("--soak-s", type=float, default=1.5, help="loaded seconds before timing (clock sampling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps

@@ -159,6 +159,8 @@ const char* fwa_last_error(void);
 int fwa_abi_version(void);
 /* Number of hot-path kernel launches this process has enqueued (bench's gpu_launches). */
 int64_t fwa_launch_count(void);
+/* Device-side error flags (synchronising read; 0 = healthy). */
+int fwa_device_flags(uint32_t* flags);
 /* Multiprocessor count and L2 bytes of the current device (for grid sizing / flushes). */
 int fwa_device_info(int32_t* sm_count, int64_t* l2_bytes);
 

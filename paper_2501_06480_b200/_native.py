@@ -114,6 +114,7 @@ _SIGNATURES = {
     "fwa_abi_version": (ctypes.c_int, []),
     "fwa_launch_count": (ctypes.c_int64, []),
     "fwa_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)]),
+    "fwa_device_flags": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32)]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
@@ -168,3 +169,9 @@ def device_info() -> tuple[int, int]:
     l2 = ctypes.c_int64(0)
     load().fwa_device_info(ctypes.byref(sm), ctypes.byref(l2))
     return int(sm.value), int(l2.value)
+
+
+def device_flags() -> int:
+    f = ctypes.c_uint32(0)
+    check(load().fwa_device_flags(ctypes.byref(f)))
+    return int(f.value)

@@ -17,6 +17,7 @@
 
 namespace fwa {
 
+__device__ unsigned int g_fwa_device_flags = 0;
 static thread_local std::string g_last_error;
 static std::atomic<int64_t> g_launches{0};
 
@@ -124,9 +125,18 @@ int pick_fwd(const fwa_desc* d, const Geom& g, bool extras, int* kernel, size_t*
   return FWA_OK;
 }
 
-int pick_bwd(const fwa_desc* d, const Geom& g, int* kernel, size_t* smem, int* tmem) {
-  if (d->kernel == FWA_KERNEL_TC)
-    return fail(FWA_ERR_CAPACITY, "tcgen05 backward is not available for this shape");
+int pick_bwd(const fwa_desc* d, const Geom& g, bool extras, bool want_dbias, int* kernel,
+             size_t* smem, int* tmem) {
+  const bool tc_ok = !want_dbias && tc_bwd_supported(g, d->dtype, extras);
+  if (d->kernel == FWA_KERNEL_TC && !tc_ok)
+    return fail(FWA_ERR_CAPACITY, "tcgen05 backward does not support this shape/dtype (L=" +
+                                      std::to_string(g.L) + ", d=" + std::to_string(g.d) + ")");
+  if (tc_ok && d->kernel != FWA_KERNEL_GENERIC) {
+    *kernel = FWA_KERNEL_TC;
+    *smem = tc_bwd_smem(g);
+    *tmem = 256;
+    return FWA_OK;
+  }
   *kernel = FWA_KERNEL_GENERIC;
   *smem = bwd_generic_smem(g);
   *tmem = 0;
@@ -145,6 +155,24 @@ using namespace fwa;
 extern "C" const char* fwa_last_error(void) { return g_last_error.c_str(); }
 extern "C" int fwa_abi_version(void) { return FWA_ABI_VERSION; }
 extern "C" int64_t fwa_launch_count(void) { return g_launches.load(); }
+
+namespace fwa {
+unsigned int* device_flags_ptr() {
+  static unsigned int* p = nullptr;
+  if (!p) {
+    void* a = nullptr;
+    if (cudaGetSymbolAddress(&a, g_fwa_device_flags) == cudaSuccess) p = (unsigned int*)a;
+  }
+  return p;
+}
+}  // namespace fwa
+
+extern "C" int fwa_device_flags(uint32_t* flags) {
+  unsigned int v = 0;
+  int rc = check_cuda(cudaMemcpyFromSymbol(&v, g_fwa_device_flags, sizeof(v)), "fwa_device_flags");
+  if (flags) *flags = v;
+  return rc;
+}
 
 extern "C" int fwa_device_info(int32_t* sm_count, int64_t* l2_bytes) {
   if (sm_count) *sm_count = device_sm_count();
@@ -171,7 +199,7 @@ extern "C" int fwa_footprint(const fwa_desc* desc, fwa_footprint_t* out) {
   out->kernel_fwd = kern;
   out->smem_bytes_fwd = (int64_t)smem;
   out->tmem_cols_fwd = tmem;
-  rc = pick_bwd(desc, g, &kern, &smem, &tmem);
+  rc = pick_bwd(desc, g, false, false, &kern, &smem, &tmem);
   if (rc) return rc;
   out->kernel_bwd = kern;
   out->smem_bytes_bwd = (int64_t)smem;
@@ -212,8 +240,10 @@ extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const
     return fail(FWA_ERR_SHAPE, "null q/k/v/dO/dq/dk/dv pointer");
   int kern = 0, tmem = 0;
   size_t smem = 0;
-  rc = pick_bwd(desc, g, &kern, &smem, &tmem);
+  rc = pick_bwd(desc, g, bias || mask, dbias != nullptr, &kern, &smem, &tmem);
   if (rc) return rc;
+  if (kern == FWA_KERNEL_TC)
+    return launch_bwd_tc(g, desc->dtype, q, k, v, dout, dq, dk, dv, (cudaStream_t)stream);
   const size_t need = fwa_bwd_workspace_bytes(desc, dbias != nullptr);
   if (need && (!workspace || workspace_bytes < need))
     return fail(FWA_ERR_CAPACITY, "backward workspace needs " + std::to_string(need) +

@@ -14,6 +14,10 @@
 
 namespace fwa {
 
+// Device-side error flags (bit 0: a TMA kernel found its dynamic smem misaligned).
+// Kernels get the address as an argument; read through fwa_device_flags().
+unsigned int* device_flags_ptr();
+
 // ---- dtype traits ---------------------------------------------------------
 template <typename T> struct DT;
 template <> struct DT<float> {
@@ -93,6 +97,12 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+
+// tcgen05 / TMA backward (fwa_tc_bwd.cu)
+bool tc_bwd_supported(const Geom& g, int dtype, bool bias_or_mask);
+size_t tc_bwd_smem(const Geom& g);
+int launch_bwd_tc(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                  const void* dout, void* dq, void* dk, void* dv, cudaStream_t s);
 
 int device_sm_count();
 int64_t device_l2_bytes();
