@@ -103,9 +103,9 @@ int validate(const fwa_desc* d, Geom* g, bool need_mask_windows_if_mask, const f
   return FWA_OK;
 }
 
-int pick_fwd(const fwa_desc* d, const Geom& g, bool extras, int* kernel, size_t* smem,
-             int* tmem) {
-  const bool tc_ok = tc_fwd_supported(g, d->dtype, extras);
+int pick_fwd(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask, int* kernel,
+             size_t* smem, int* tmem) {
+  const bool tc_ok = tc_fwd_supported(g, d->dtype, has_bias, has_mask);
   if (d->kernel == FWA_KERNEL_TC && !tc_ok)
     return fail(FWA_ERR_CAPACITY, "tcgen05 forward does not support this shape/dtype (L=" +
                                       std::to_string(g.L) + ", d=" + std::to_string(g.d) + ")");
@@ -194,7 +194,7 @@ extern "C" int fwa_footprint(const fwa_desc* desc, fwa_footprint_t* out) {
   out->hbm_bytes_bwd = 7 * lcd;
   size_t smem = 0;
   int kern = 0, tmem = 0;
-  rc = pick_fwd(desc, g, false, &kern, &smem, &tmem);
+  rc = pick_fwd(desc, g, false, false, &kern, &smem, &tmem);
   if (rc) return rc;
   out->kernel_fwd = kern;
   out->smem_bytes_fwd = (int64_t)smem;
@@ -215,7 +215,7 @@ extern "C" int fwa_fwd(const fwa_desc* desc, const void* q, const void* k, const
   if (!q || !k || !v || !o) return fail(FWA_ERR_SHAPE, "null q/k/v/o pointer");
   int kern = 0, tmem = 0;
   size_t smem = 0;
-  rc = pick_fwd(desc, g, bias || mask, &kern, &smem, &tmem);
+  rc = pick_fwd(desc, g, bias != nullptr, mask != nullptr, &kern, &smem, &tmem);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (kern == FWA_KERNEL_TC) return launch_fwd_tc(g, desc->dtype, q, k, v, bias, mask, o, s);

@@ -69,7 +69,7 @@ bool bwd_generic_fits(const Geom& g);
 int bwd_generic_grid(const Geom& g);
 
 // tcgen05 / TMA forward (fwa_tc_fwd.cu)
-bool tc_fwd_supported(const Geom& g, int dtype, bool bias_or_mask);
+bool tc_fwd_supported(const Geom& g, int dtype, bool has_bias, bool has_mask);
 size_t tc_fwd_smem(const Geom& g, int dtype);
 int tc_fwd_tmem_cols(const Geom& g);
 int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k,

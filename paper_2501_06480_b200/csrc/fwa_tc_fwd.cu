@@ -9,15 +9,15 @@
 //     rows L..63 are out of bounds and arrive as zeros, so L = 49 needs no
 //     host padding, and the swizzled smem image is exactly the UMMA
 //     K-major (Q, K) / MN-major (V) canonical layout.
-//   * S = Q K^T: one tcgen05.mma chain (M=128, N=128, K=d) into TMEM columns
-//     [0,128). Only the two diagonal 64x64 blocks are used.
+//   * S = Q K^T: two tcgen05.mma chains (M=128, N=64, K=d), one per unit, with
+//     complementary disable-output-lane masks, so both units' scores share TMEM
+//     columns [0,64) (unit 0 in lanes 0-63, unit 1 in lanes 64-127).
 //   * Softmax: 4 warps, one thread per row (TMEM lane = row): tcgen05.ld of the
 //     row's own 64-column block, masked max over the L valid keys, ex2, row
 //     sum; P (unnormalised, f16/bf16 pairs) is written back to TMEM with
-//     tcgen05.st (columns [128,192); the other unit's half of each row stays
-//     zero), so P never touches shared memory.
-//   * O = P V: tcgen05.mma with A from TMEM (M=128, N=d, K=128) into TMEM
-//     (double-buffered O at [192, 192+2d)).
+//     tcgen05.st (columns [64,96)), so P never touches shared memory.
+//   * O = P V: per unit a lane-masked tcgen05.mma with A from TMEM (M=128, N=d,
+//     K=64) into TMEM (double-buffered O at [96, 96+2d)).
 //   * Shared memory holds only the TMA ring (4 stages for d=32, 8 for d=16)
 //     and one staging tile for the TMA store.
 //   * Epilogue: tcgen05.ld, scale by 1/rowsum, convert, swizzled staging,
@@ -60,9 +60,12 @@ struct Cfg {
   static constexpr int kSmem = 1024 /*align slack*/ + kStages * 3 * kTileBytes +
                                kTileBytes /*O staging*/ + 256 /*barriers*/;
   static constexpr int kChunks = kRowBytes / 16;  // 16-byte chunks per row
-  // TMEM columns: S [0,128) fp32 | P [128,192) 16-bit pairs | O0, O1 (d each) fp32
-  static constexpr uint32_t kTmemP = 128, kTmemO0 = 192, kTmemO1 = 192 + D;
-  static constexpr uint32_t kTmemCols = 192 + 2 * D <= 256 ? 256 : 512;
+  // TMEM columns (lane = tile row; unit 0 rows are lanes 0-63, unit 1 rows 64-127):
+  //   S [0,64) fp32 | P [64,96) 16-bit pairs | O0, O1 (d each) fp32.
+  // Each unit's S/P/O occupy the SAME columns in its own 64 lanes: the MMAs for
+  // unit 0 and unit 1 run with complementary disable-output-lane masks.
+  static constexpr uint32_t kTmemP = 64, kTmemO0 = 96, kTmemO1 = 96 + D;
+  static constexpr uint32_t kTmemCols = 256;
 };
 
 struct SmemBarriers {
@@ -73,12 +76,22 @@ struct SmemBarriers {
   uint32_t tmem_base;
 };
 
+// Additive bias/mask: the grid is a multiple of the (window mod nW, head) period
+// of the tile sequence, so every tile of a CTA sees the same two (w, h) pairs and
+// each thread keeps its row of (bias + mask) * log2(e) in registers (f16 pairs).
+struct AddArgs {
+  const float* bias;  // [heads][L][L] or null
+  const float* mask;  // [nW][L][L] or null
+  int heads;
+  int mask_windows;
+};
+
 // LK > 0: compile-time window length (Swin 7x7 / 8x8); LK == 0: runtime L.
-template <typename T, int D, int LK>
+template <typename T, int D, int LK, bool ADD>
 __global__ void __launch_bounds__(kThreads, Cfg<D>::kCtasPerSm)
 fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-              int n_tiles, int L_rt, float scale_log2) {
+              int n_tiles, int L_rt, float scale_log2, AddArgs add) {
   using C = Cfg<D>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   const int L = LK > 0 ? LK : L_rt;
@@ -143,7 +156,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0 && n_local > 0) {
-      constexpr uint32_t idS = make_idesc_f16(kBF16, 128, 128, false, false);
+      constexpr uint32_t idS = make_idesc_f16(kBF16, 128, 64, false, false);
       constexpr uint32_t idO = make_idesc_f16(kBF16, 128, D, false, true);
       constexpr uint32_t sbo_qk = 8 * C::kRowBytes;  // 8-row core-matrix group stride
       auto issue_S = [&](int i) {
@@ -151,10 +164,14 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         const uint32_t q0 = smem_u32(sQ + st * C::kTileBytes);
         const uint32_t k0 = smem_u32(sK + st * C::kTileBytes);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t a = make_sdesc(q0 + kk * 32, 16, sbo_qk, C::kSwz);
-          const uint64_t b = make_sdesc(k0 + kk * 32, 16, sbo_qk, C::kSwz);
-          mma_f16_ss(tmem, a, b, idS, kk > 0);
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t lo = u ? ~0u : 0u, hi = u ? 0u : ~0u;  // unit u writes lanes 64u..64u+63
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t a = make_sdesc(q0 + kk * 32, 16, sbo_qk, C::kSwz);
+            const uint64_t b = make_sdesc(k0 + u * 64 * C::kRowBytes + kk * 32, 16, sbo_qk, C::kSwz);
+            mma_f16_ss_m(tmem, a, b, idS, kk > 0, lo, lo, hi, hi);
+          }
         }
         mma_commit(&bars->s_full);
       };
@@ -179,10 +196,14 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         const uint32_t v0 = smem_u32(sV + st * C::kTileBytes);
         const uint32_t od = tmem + (ob ? C::kTmemO1 : C::kTmemO0);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t b = make_sdesc(v0 + kk * 16 * C::kRowBytes, C::kTileBytes,
-                                        8 * C::kRowBytes, C::kSwz);
-          mma_f16_ts(od, tmem + C::kTmemP + kk * 8, b, idO, kk > 0);
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t lo = u ? ~0u : 0u, hi = u ? 0u : ~0u;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t b = make_sdesc(v0 + (u * 64 + kk * 16) * C::kRowBytes, C::kTileBytes,
+                                          8 * C::kRowBytes, C::kSwz);
+            mma_f16_ts_m(od, tmem + C::kTmemP + kk * 8, b, idO, kk > 0, lo, lo, hi, hi);
+          }
         }
         mma_commit(&bars->pv_done[ob]);
         mma_commit(&bars->empty[st]);
@@ -197,13 +218,24 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
     uint8_t* orow = sO + row * C::kRowBytes;
     const uint32_t oswz = (uint32_t)((row * C::kRowBytes) >> 7) & (C::kChunks - 1);
     const bool leader = (threadIdx.x == 64);
-    // the other unit's 32 P columns of this row stay zero for the whole kernel
-    {
-      uint32_t z[32];
+    uint32_t addh[ADD ? 32 : 1];
+    if constexpr (ADD) {
+      const int r_in = row & 63;
+      const int u0 = 2 * (int)blockIdx.x + ul;  // same (w, h) for every tile of this CTA
+      const int hd = u0 % add.heads;
+      const int w = (u0 / add.heads) % add.mask_windows;
+      const float* brow = add.bias ? add.bias + ((size_t)hd * L + r_in) * L : nullptr;
+      const float* mrow = add.mask ? add.mask + ((size_t)w * L + r_in) * L : nullptr;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) z[j] = 0u;
-      tmem_st32(tmem + t_lane + C::kTmemP + (1 - ul) * 32, z);
-      tmem_wait_st();
+      for (int j = 0; j < 64; j += 2) {
+        float a = 0.f, b = 0.f;
+        if (r_in < L) {
+          if (j < L) a = ((brow ? brow[j] : 0.f) + (mrow ? mrow[j] : 0.f)) * 1.4426950408889634f;
+          if (j + 1 < L) b = ((brow ? brow[j + 1] : 0.f) + (mrow ? mrow[j + 1] : 0.f)) * 1.4426950408889634f;
+        }
+        __half2 h2 = __floats2half2_rn(a, b);
+        addh[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+      }
     }
     float inv_prev = 0.f;
     for (int i = 0; i <= n_local; ++i) {
@@ -215,22 +247,36 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
 #pragma unroll
         for (int g = 0; g < 4; ++g)
           if (LK == 0 || g * 16 < LK)
-            tmem_ld16(tmem + t_lane + ul * 64 + g * 16,
-                      *reinterpret_cast<uint32_t(*)[16]>(&s[g * 16]));
+            tmem_ld16(tmem + t_lane + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&s[g * 16]));
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&bars->s_empty);
         float mx = -INFINITY;
+        if constexpr (ADD) {
+          // t = scale*log2e*S + (bias+mask)*log2e, kept in s[]
 #pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (j < L) mx = fmaxf(mx, __uint_as_float(s[j]));
-        const float mxs = mx * scale_log2;
+          for (int j = 0; j < 64; j += 2) {
+            const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&addh[j >> 1]));
+            const float t0 = fmaf(__uint_as_float(s[j]), scale_log2, a.x);
+            const float t1 = fmaf(__uint_as_float(s[j + 1]), scale_log2, a.y);
+            s[j] = __float_as_uint(t0);
+            s[j + 1] = __float_as_uint(t1);
+            if (j < L) mx = fmaxf(mx, t0);
+            if (j + 1 < L) mx = fmaxf(mx, t1);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < L) mx = fmaxf(mx, __uint_as_float(s[j]));
+        }
+        const float mxs = ADD ? mx : mx * scale_log2;
+        const float sl2 = ADD ? 1.f : scale_log2;
         float sum = 0.f;
         uint32_t pk[32];
 #pragma unroll
         for (int j = 0; j < 64; j += 2) {
-          const float p0 = j < L ? ex2(fmaf(__uint_as_float(s[j]), scale_log2, -mxs)) : 0.f;
-          const float p1 = j + 1 < L ? ex2(fmaf(__uint_as_float(s[j + 1]), scale_log2, -mxs)) : 0.f;
+          const float p0 = j < L ? ex2(fmaf(__uint_as_float(s[j]), sl2, -mxs)) : 0.f;
+          const float p1 = j + 1 < L ? ex2(fmaf(__uint_as_float(s[j + 1]), sl2, -mxs)) : 0.f;
           sum += p0 + p1;
           if constexpr (kBF16) {
             __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
@@ -246,7 +292,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
           mbar_wait(&bars->pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
           tc_fence_after();
         }
-        tmem_st32(tmem + t_lane + C::kTmemP + ul * 32, pk);
+        tmem_st32(tmem + t_lane + C::kTmemP, pk);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->p_full);
@@ -302,16 +348,24 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
 }
 
 // ---- host side ---------------------------------------------------------------
-template <typename T, int D, int LK>
+// Period (in tiles) after which the (window mod nW, head) pair of a tile slot repeats.
+int add_period_tiles(const Geom& g, bool has_bias, bool has_mask) {
+  if (!has_bias && !has_mask) return 1;
+  const int64_t pu = (int64_t)g.heads * (has_mask ? g.mask_windows : 1);
+  const int64_t pt = (pu % 2 == 0) ? pu / 2 : pu;
+  return pt > (1 << 30) ? (1 << 30) : (int)pt;
+}
+
+template <typename T, int D, int LK, bool ADD>
 int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
-             cudaStream_t s) {
+             const float* bias, const float* mask, cudaStream_t s) {
   CUtensorMap mq, mk, mv, mo;
   int rc;
   if ((rc = get_units_map(&mq, q, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
   if ((rc = get_units_map(&mk, k, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
   if ((rc = get_units_map(&mv, v, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
   if ((rc = get_units_map(&mo, o, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
-  auto kern = fwd_tc_kernel<T, D, LK>;
+  auto kern = fwd_tc_kernel<T, D, LK, ADD>;
   constexpr int smem = Cfg<D>::kSmem;
   static bool attr_done = false;
   if (!attr_done) {
@@ -322,40 +376,53 @@ int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void*
   }
   const int n_tiles = (int)((g.units + 1) / 2);
   const int per_sm = Cfg<D>::kCtasPerSm;
-  const int grid = std::max(1, std::min(n_tiles, device_sm_count() * per_sm));
+  int grid = std::max(1, std::min(n_tiles, device_sm_count() * per_sm));
+  if (ADD && n_tiles > grid) {
+    const int pt = add_period_tiles(g, bias != nullptr, mask != nullptr);
+    grid = (grid / pt) * pt;  // tc_fwd_supported guarantees pt <= grid
+  }
   const float scale_log2 = g.scale * 1.4426950408889634f;
+  AddArgs add{bias, mask, g.heads, mask ? g.mask_windows : 1};
   rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, mq, mk, mv, mo, n_tiles,
-                             (int)g.L, scale_log2),
+                             (int)g.L, scale_log2, add),
                   "fwd_tc_kernel launch");
   if (rc) return rc;
   count_launch();
   return check_cuda(cudaGetLastError(), "fwd_tc_kernel launch");
 }
 
-template <typename T, int D>
+template <typename T, int D, bool ADD>
 int dispatch_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
-               cudaStream_t s) {
-  if (g.L == 49) return launch_t<T, D, 49>(g, dtype, q, k, v, o, s);
-  if (g.L == 64) return launch_t<T, D, 64>(g, dtype, q, k, v, o, s);
-  return launch_t<T, D, 0>(g, dtype, q, k, v, o, s);
+               const float* b, const float* m, cudaStream_t s) {
+  if (g.L == 49) return launch_t<T, D, 49, ADD>(g, dtype, q, k, v, o, b, m, s);
+  if (g.L == 64) return launch_t<T, D, 64, ADD>(g, dtype, q, k, v, o, b, m, s);
+  return launch_t<T, D, 0, ADD>(g, dtype, q, k, v, o, b, m, s);
 }
 
 template <typename T>
 int dispatch_d(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
-               cudaStream_t s) {
+               const float* b, const float* m, cudaStream_t s) {
+  const bool add = b || m;
   switch (g.d) {
-    case 16: return dispatch_l<T, 16>(g, dtype, q, k, v, o, s);
-    case 32: return dispatch_l<T, 32>(g, dtype, q, k, v, o, s);
-    case 64: return dispatch_l<T, 64>(g, dtype, q, k, v, o, s);
+    case 16: return add ? dispatch_l<T, 16, true>(g, dtype, q, k, v, o, b, m, s)
+                        : dispatch_l<T, 16, false>(g, dtype, q, k, v, o, b, m, s);
+    case 32: return add ? dispatch_l<T, 32, true>(g, dtype, q, k, v, o, b, m, s)
+                        : dispatch_l<T, 32, false>(g, dtype, q, k, v, o, b, m, s);
+    case 64: return add ? dispatch_l<T, 64, true>(g, dtype, q, k, v, o, b, m, s)
+                        : dispatch_l<T, 64, false>(g, dtype, q, k, v, o, b, m, s);
   }
   return fail(FWA_ERR_CAPACITY, "tcgen05 forward: unsupported head_dim");
 }
 
 }  // namespace
 
-bool tc_fwd_supported(const Geom& g, int dtype, bool bias_or_mask) {
-  if (bias_or_mask) return false;  // bias/mask shapes run on the generic kernel for now
+bool tc_fwd_supported(const Geom& g, int dtype, bool has_bias, bool has_mask) {
   if (dtype != FWA_F16 && dtype != FWA_BF16) return false;
+  if (has_bias || has_mask) {
+    const int64_t n_tiles = (g.units + 1) / 2;
+    const int cap = device_sm_count() * (g.d <= 32 ? 2 : 1);
+    if (n_tiles > cap && add_period_tiles(g, has_bias, has_mask) > cap) return false;
+  }
   if (g.L < 1 || g.L > kUnitRows) return false;
   if (g.d != 16 && g.d != 32 && g.d != 64) return false;
   if (g.units > (int64_t)1 << 31) return false;
@@ -372,10 +439,9 @@ int tc_fwd_tmem_cols(const Geom& g) {
 
 int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                   const float* bias, const float* mask, void* o, cudaStream_t s) {
-  if (bias || mask) return fail(FWA_ERR_CAPACITY, "tcgen05 forward: bias/mask not supported yet");
   const bool bf = dtype == FWA_BF16;
-  return bf ? dispatch_d<__nv_bfloat16>(g, dtype, q, k, v, o, s)
-            : dispatch_d<__half>(g, dtype, q, k, v, o, s);
+  return bf ? dispatch_d<__nv_bfloat16>(g, dtype, q, k, v, o, bias, mask, s)
+            : dispatch_d<__half>(g, dtype, q, k, v, o, bias, mask, s);
   return fail(FWA_ERR_CAPACITY, "tcgen05 forward: unsupported head_dim");
 }
 

@@ -283,6 +283,40 @@ def test_tc_backward_does_not_write_outside_outputs():
     assert dk.float().sum(dim=2).abs().max().item() < 2e-2
 
 
+def _torch_ref(q, k, v, scale, bias=None, mask=None):
+    s = (q.float() @ k.float().transpose(-1, -2)) * scale
+    if bias is not None:
+        s = s + bias[None]
+    if mask is not None:
+        nW = mask.shape[0]
+        s = s + mask[torch.arange(q.shape[0], device=q.device) % nW][:, None]
+    return torch.softmax(s, -1) @ v.float()
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("N,h,L,d,nW,use_bias", [
+    (8192, 3, 49, 32, 64, True),    # Swin-T stage 1, shifted layer: period 96 tiles
+    (2048, 6, 49, 32, 16, True),
+    (128, 24, 49, 32, 0, True),     # stage 4: bias only
+    (3000, 5, 49, 16, 7, True),     # odd period (35 tiles)
+    (1500, 3, 64, 64, 0, True),     # bias only, d=64 (1 CTA/SM)
+    (999, 2, 36, 32, 9, False),     # mask only
+    (600, 1, 49, 32, 300, True),    # period (150) above the grid cap -> generic kernel
+])
+def test_forward_bias_mask_full_size(dt, N, h, L, d, nW, use_bias):
+    dtype = DTYPES[dt]
+    rng = fwa.Rng(N + h)
+    q, k, v = (fwa.fill_uniform(rng, (N, h, L, d), dtype=dtype) for _ in range(3))
+    bias = fwa.fill_uniform(rng, (h, L, L), -1.0, 1.0) if use_bias else None
+    mask = None
+    if nW:
+        mask = torch.where(fwa.fill_uniform(rng, (nW, L, L)) > 0.4, -100.0, 0.0).float().contiguous()
+    o = ops.attention_forward(q, k, v, d ** -0.5, bias, mask)
+    ref = _torch_ref(q, k, v, d ** -0.5, bias, mask)
+    assert (o.float() - ref).abs().max().item() <= 2e-2
+    assert fwa._native.device_flags() == 0
+
+
 def test_footprint_reports_kernel_and_paper_peaks():
     fp = ops.footprint(8192, 3, 49, 32, torch.float16, chunks=2)
     assert fp["paper_peak_fwd"] == (49 * 49 + 2 * 49 * 16) * 2
