@@ -125,16 +125,16 @@ int pick_fwd(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask, int
   return FWA_OK;
 }
 
-int pick_bwd(const fwa_desc* d, const Geom& g, bool extras, bool want_dbias, int* kernel,
-             size_t* smem, int* tmem) {
-  const bool tc_ok = !want_dbias && tc_bwd_supported(g, d->dtype, extras);
+int pick_bwd(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask, bool want_dbias,
+             int* kernel, size_t* smem, int* tmem) {
+  const bool tc_ok = tc_bwd_supported(g, d->dtype, has_bias, has_mask, want_dbias);
   if (d->kernel == FWA_KERNEL_TC && !tc_ok)
     return fail(FWA_ERR_CAPACITY, "tcgen05 backward does not support this shape/dtype (L=" +
                                       std::to_string(g.L) + ", d=" + std::to_string(g.d) + ")");
   if (tc_ok && d->kernel != FWA_KERNEL_GENERIC) {
     *kernel = FWA_KERNEL_TC;
     *smem = tc_bwd_smem(g);
-    *tmem = 256;
+    *tmem = tc_bwd_tmem_cols(g);
     return FWA_OK;
   }
   *kernel = FWA_KERNEL_GENERIC;
@@ -199,7 +199,7 @@ extern "C" int fwa_footprint(const fwa_desc* desc, fwa_footprint_t* out) {
   out->kernel_fwd = kern;
   out->smem_bytes_fwd = (int64_t)smem;
   out->tmem_cols_fwd = tmem;
-  rc = pick_bwd(desc, g, false, false, &kern, &smem, &tmem);
+  rc = pick_bwd(desc, g, false, false, false, &kern, &smem, &tmem);
   if (rc) return rc;
   out->kernel_bwd = kern;
   out->smem_bytes_bwd = (int64_t)smem;
@@ -226,7 +226,10 @@ extern "C" size_t fwa_bwd_workspace_bytes(const fwa_desc* desc, int want_dbias) 
   Geom g;
   if (validate(desc, &g, false, nullptr)) return 0;
   if (!want_dbias) return 0;
-  return (size_t)bwd_generic_grid(g) * g.heads * g.L * g.L * sizeof(float);
+  g.mask_windows = desc->mask_windows > 0 ? desc->mask_windows : 1;
+  const size_t generic = (size_t)bwd_generic_grid(g) * g.heads * g.L * g.L * sizeof(float);
+  const size_t tc = tc_bwd_workspace_bytes(g, desc->mask_windows > 0, true);
+  return generic > tc ? generic : tc;
 }
 
 extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const void* v,
@@ -240,14 +243,15 @@ extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const
     return fail(FWA_ERR_SHAPE, "null q/k/v/dO/dq/dk/dv pointer");
   int kern = 0, tmem = 0;
   size_t smem = 0;
-  rc = pick_bwd(desc, g, bias || mask, dbias != nullptr, &kern, &smem, &tmem);
+  rc = pick_bwd(desc, g, bias != nullptr, mask != nullptr, dbias != nullptr, &kern, &smem, &tmem);
   if (rc) return rc;
-  if (kern == FWA_KERNEL_TC)
-    return launch_bwd_tc(g, desc->dtype, q, k, v, dout, dq, dk, dv, (cudaStream_t)stream);
   const size_t need = fwa_bwd_workspace_bytes(desc, dbias != nullptr);
   if (need && (!workspace || workspace_bytes < need))
     return fail(FWA_ERR_CAPACITY, "backward workspace needs " + std::to_string(need) +
                                       " bytes, got " + std::to_string(workspace_bytes));
+  if (kern == FWA_KERNEL_TC)
+    return launch_bwd_tc(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
+                         (float*)workspace, (cudaStream_t)stream);
   return launch_bwd_generic(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
                             (float*)workspace, (cudaStream_t)stream);
 }

@@ -99,10 +99,13 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }
 
 // tcgen05 / TMA backward (fwa_tc_bwd.cu)
-bool tc_bwd_supported(const Geom& g, int dtype, bool bias_or_mask);
+bool tc_bwd_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias);
 size_t tc_bwd_smem(const Geom& g);
+int tc_bwd_tmem_cols(const Geom& g);
+size_t tc_bwd_workspace_bytes(const Geom& g, bool has_mask, bool want_dbias);
 int launch_bwd_tc(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                  const void* dout, void* dq, void* dk, void* dv, cudaStream_t s);
+                  const void* dout, const float* bias, const float* mask, void* dq, void* dk,
+                  void* dv, float* dbias, float* ws, cudaStream_t s);
 
 int device_sm_count();
 int64_t device_l2_bytes();

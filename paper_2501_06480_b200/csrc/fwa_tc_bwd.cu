@@ -6,14 +6,18 @@
 //
 //   S  = Q K^T          tcgen05 SS, M=128 N=128 K=d  -> TMEM [0,128)
 //   dP = dO V^T         tcgen05 SS, M=128 N=128 K=d  -> TMEM [128,256)
-//   softmax warps (thread = query row = TMEM lane): P = softmax(scale*S),
-//     rho = sum_j P dP, dS = scale * P (dP - rho)  (flash.py:133-138, :241-242);
-//     P and dS go to shared memory as [query][key] SW128 tiles (the two
-//     off-diagonal 64x64 blocks share one zero block).
+//   (every MMA is issued once per unit with complementary disable-output-lane
+//   masks, so both units share TMEM columns: S [0,64), dP [64,128))
+//   softmax warps (thread = query row = TMEM lane): P = softmax(scale*S [+bias
+//     +mask]), rho = sum_j P dP, dS = scale * P (dP - rho)  (flash.py:133-138,
+//     :241-242); P and dS go to shared memory as [query][64 keys] SW128 tiles.
+//     With dBias requested, P (dP - rho) is accumulated per CTA in TMEM [128,192)
+//     (the grid is period-aligned so every tile of a CTA has the same heads) and
+//     reduced over CTAs in a fixed order afterwards (deterministic).
 //   dV = P^T dO         A = P read MN-major (the same bytes), B = dO MN-major
 //   dK = dS^T Q         A = dS MN-major, B = Q MN-major
 //   dQ = dS K           A = dS K-major, B = K MN-major
-//   (gradient accumulators reuse TMEM [0, 3d) once S and dP are in registers)
+//   (gradient accumulators reuse the S/dP columns once they are in registers)
 //   Epilogue: tcgen05.ld of dV/dK/dQ rows, convert, stage into the tile's own
 //   (now dead) Q/K/V smem slots, three TMA stores; the stage is released to the
 //   producer only after the stores have read the staging.
@@ -37,7 +41,7 @@ using namespace sm100;
 constexpr int kThreads = 192;
 constexpr int kTileRows = 128;
 constexpr int kUnitRows = 64;
-constexpr int kPBytes = 24 * 1024;  // [u0 | zero | u1] SW128 tile
+constexpr int kPBytes = 16 * 1024;  // [128 query rows][64 keys of the row's own unit], SW128
 
 template <int D>
 struct BCfg {
@@ -49,8 +53,12 @@ struct BCfg {
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
   static constexpr int kSmem = kStages * kStageBytes + 2 * kPBytes + 256;
   static constexpr int kChunks = kRowBytes / 16;
-  static constexpr uint32_t kTmemCols = 256;
-  static constexpr uint32_t kTdP = 128, kTdV = 0, kTdK = D, kTdQ = 2 * D;
+  // TMEM (lane = tile row): S [0,64) | dP [64,128) | dBias acc [128,192) |
+  // gradients dV, dK, dQ at [0,3d) when they fit in the S/dP columns, else [192,192+3d).
+  static constexpr uint32_t kTdP = 64, kTdB = 128;
+  static constexpr uint32_t kTg = 3 * D <= 128 ? 0 : 192;
+  static constexpr uint32_t kTdV = kTg, kTdK = kTg + D, kTdQ = kTg + 2 * D;
+  static constexpr uint32_t kTmemCols = kTg + 3 * D <= 256 ? 256 : 512;
 };
 
 struct BwdBarriers {
@@ -58,6 +66,14 @@ struct BwdBarriers {
   uint64_t empty[4];
   uint64_t s_full, p_ready, ds_ready, grad_done, grad_free;
   uint32_t tmem_base;
+};
+
+struct BwdAddArgs {
+  const float* bias;   // [heads][L][L] or null
+  const float* mask;   // [nW][L][L] or null
+  float* dbias_ws;     // [grid][128][64] per-CTA dS partials (DBIAS) or null
+  int heads;
+  int mask_windows;
 };
 
 template <typename T>
@@ -71,12 +87,13 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   }
 }
 
-template <typename T, int D, int LK>
+template <typename T, int D, int LK, bool ADD, bool DBIAS>
 __global__ void __launch_bounds__(kThreads, BCfg<D>::kCtasPerSm)
 bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
               const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dk,
-              const __grid_constant__ CUtensorMap tm_dv, int n_tiles, int L_rt, float scale, unsigned int* err_flags) {
+              const __grid_constant__ CUtensorMap tm_dv, int n_tiles, int L_rt, float scale,
+              BwdAddArgs add, unsigned int* err_flags) {
   using C = BCfg<D>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   const int L = LK > 0 ? LK : L_rt;
@@ -96,6 +113,7 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
+  // key chunks >= ceil(L/8) of P and dS are never written: they must read as zero
   for (int i = threadIdx.x; i < 2 * kPBytes / 16; i += kThreads)
     reinterpret_cast<uint4*>(sP)[i] = make_uint4(0, 0, 0, 0);
   fence_proxy_async_smem();
@@ -146,55 +164,67 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
+    // ===================== MMA issuer (per unit, complementary lane masks) =====================
     if (lane == 0) {
-      constexpr uint32_t idS = make_idesc_f16(kBF16, 128, 128, false, false);
+      constexpr uint32_t idS = make_idesc_f16(kBF16, 128, 64, false, false);
       constexpr uint32_t idMN = make_idesc_f16(kBF16, 128, D, true, true);    // dV, dK
       constexpr uint32_t idQ = make_idesc_f16(kBF16, 128, D, false, true);    // dQ
       constexpr uint32_t sbo_row = 8 * C::kRowBytes;
+      constexpr uint32_t kUnitBytes = kUnitRows * C::kRowBytes;  // 64 rows of one unit
       const uint32_t p0 = smem_u32(sP), ds0 = smem_u32(sDS);
       for (int i = 0; i < n_local; ++i) {
         const int st = i % C::kStages;
         const uint32_t q0 = smem_u32(slot(st, 0)), k0 = smem_u32(slot(st, 1));
         const uint32_t v0 = smem_u32(slot(st, 2)), do0 = smem_u32(slot(st, 3));
         mbar_wait(&bars->full[st], (i / C::kStages) & 1);
-        if (i > 0) mbar_wait(&bars->grad_free, (i - 1) & 1);  // TMEM [0,256) free again
+        if (i > 0) mbar_wait(&bars->grad_free, (i - 1) & 1);  // S/dP/gradient columns free
         tc_fence_after();
-        // S = Q K^T, dP = dO V^T (both operands K-major, K = d)
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          mma_f16_ss(tmem, make_sdesc(q0 + kk * 32, 16, sbo_row, C::kSwz),
-                     make_sdesc(k0 + kk * 32, 16, sbo_row, C::kSwz), idS, kk > 0);
-        }
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t lo = u ? ~0u : 0u, hi = u ? 0u : ~0u;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          mma_f16_ss(tmem + C::kTdP, make_sdesc(do0 + kk * 32, 16, sbo_row, C::kSwz),
-                     make_sdesc(v0 + kk * 32, 16, sbo_row, C::kSwz), idS, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk)   // S_u = Q K_u^T
+            mma_f16_ss_m(tmem, make_sdesc(q0 + kk * 32, 16, sbo_row, C::kSwz),
+                         make_sdesc(k0 + u * kUnitBytes + kk * 32, 16, sbo_row, C::kSwz), idS,
+                         kk > 0, lo, lo, hi, hi);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)   // dP_u = dO V_u^T
+            mma_f16_ss_m(tmem + C::kTdP, make_sdesc(do0 + kk * 32, 16, sbo_row, C::kSwz),
+                         make_sdesc(v0 + u * kUnitBytes + kk * 32, 16, sbo_row, C::kSwz), idS,
+                         kk > 0, lo, lo, hi, hi);
         }
         mma_commit(&bars->s_full);
-        // dV = P^T dO   (K = query rows; A = P read MN-major, B = dO MN-major)
+        // dV_u = P_u^T dO_u : A = P read MN-major (M = key, K = query; atom 1 = unit-1 rows)
         mbar_wait(&bars->p_ready, i & 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_f16_ss(tmem + C::kTdV, make_sdesc(p0 + kk * 2048, 8192, 1024, 2),
-                     make_sdesc(do0 + kk * 16 * C::kRowBytes, C::kTileBytes, sbo_row, C::kSwz),
-                     idMN, kk > 0);
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t lo = u ? ~0u : 0u, hi = u ? 0u : ~0u;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_f16_ss_m(tmem + C::kTdV, make_sdesc(p0 + kk * 2048, 8192, 1024, 2),
+                         make_sdesc(do0 + u * kUnitBytes + kk * 16 * C::kRowBytes, C::kTileBytes,
+                                    sbo_row, C::kSwz),
+                         idMN, kk > 0, lo, lo, hi, hi);
         }
-        // dK = dS^T Q ; dQ = dS K
+        // dK_u = dS_u^T Q_u ; dQ_u = dS_u K_u
         mbar_wait(&bars->ds_ready, i & 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_f16_ss(tmem + C::kTdK, make_sdesc(ds0 + kk * 2048, 8192, 1024, 2),
-                     make_sdesc(q0 + kk * 16 * C::kRowBytes, C::kTileBytes, sbo_row, C::kSwz),
-                     idMN, kk > 0);
-        }
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t lo = u ? ~0u : 0u, hi = u ? 0u : ~0u;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_f16_ss(tmem + C::kTdQ, make_sdesc(ds0 + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024, 2),
-                     make_sdesc(k0 + kk * 16 * C::kRowBytes, C::kTileBytes, sbo_row, C::kSwz),
-                     idQ, kk > 0);
+          for (int kk = 0; kk < 4; ++kk)
+            mma_f16_ss_m(tmem + C::kTdK, make_sdesc(ds0 + kk * 2048, 8192, 1024, 2),
+                         make_sdesc(q0 + u * kUnitBytes + kk * 16 * C::kRowBytes, C::kTileBytes,
+                                    sbo_row, C::kSwz),
+                         idMN, kk > 0, lo, lo, hi, hi);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_f16_ss_m(tmem + C::kTdQ, make_sdesc(ds0 + kk * 32, 16, 1024, 2),
+                         make_sdesc(k0 + u * kUnitBytes + kk * 16 * C::kRowBytes, C::kTileBytes,
+                                    sbo_row, C::kSwz),
+                         idQ, kk > 0, lo, lo, hi, hi);
         }
         mma_commit(&bars->grad_done);
       }
@@ -204,13 +234,40 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int ul = row >> 6;
+    const int r_in = row & 63;
     const uint32_t t_lane = (uint32_t)(q * 32) << 16;
     const uint32_t pswz = (uint32_t)(row & 7);
-    const int prow_off = ul * 8192 + (row >> 3) * 1024 + (row & 7) * 128;
+    const int prow_off = (row >> 3) * 1024 + (row & 7) * 128;
     const uint32_t oswz = (uint32_t)((row * C::kRowBytes) >> 7) & (C::kChunks - 1);
     const bool leader = (threadIdx.x == 64);
     const int p_chunks = LK > 0 ? (LK + 7) / 8 : 8;
     const float scale_log2 = scale * 1.4426950408889634f;
+    uint32_t addh[ADD ? 32 : 1];
+    if constexpr (ADD) {
+      const int u0 = 2 * (int)blockIdx.x + ul;  // same (w, h) for every tile of this CTA
+      const int hd = u0 % add.heads;
+      const int w = (u0 / add.heads) % add.mask_windows;
+      const float* brow = add.bias ? add.bias + ((size_t)hd * L + r_in) * L : nullptr;
+      const float* mrow = add.mask ? add.mask + ((size_t)w * L + r_in) * L : nullptr;
+#pragma unroll
+      for (int j = 0; j < 64; j += 2) {
+        float a = 0.f, b = 0.f;
+        if (r_in < L) {
+          if (j < L) a = ((brow ? brow[j] : 0.f) + (mrow ? mrow[j] : 0.f)) * 1.4426950408889634f;
+          if (j + 1 < L) b = ((brow ? brow[j + 1] : 0.f) + (mrow ? mrow[j + 1] : 0.f)) * 1.4426950408889634f;
+        }
+        __half2 h2 = __floats2half2_rn(a, b);
+        addh[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+    }
+    if constexpr (DBIAS) {
+      uint32_t z[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z[j] = 0u;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) tmem_st16(tmem + t_lane + C::kTdB + g * 16, z);
+      tmem_wait_st();
+    }
     for (int i = 0; i < n_local; ++i) {
       const int tile = blockIdx.x + i * gridDim.x;
       const int st = i % C::kStages;
@@ -220,22 +277,35 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         if (LK == 0 || g * 16 < LK) {
-          tmem_ld16(tmem + t_lane + ul * 64 + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&s[g * 16]));
-          tmem_ld16(tmem + t_lane + C::kTdP + ul * 64 + g * 16,
-                    *reinterpret_cast<uint32_t(*)[16]>(&dp[g * 16]));
+          tmem_ld16(tmem + t_lane + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&s[g * 16]));
+          tmem_ld16(tmem + t_lane + C::kTdP + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&dp[g * 16]));
         }
       }
       tmem_wait_ld();
-      // P = softmax(scale * S) over the L valid keys (normalised: dV needs true P)
+      // P = softmax(scale*S [+ bias + mask]) over the L valid keys (normalised: dV needs true P)
       float mx = -INFINITY;
+      if constexpr (ADD) {
 #pragma unroll
-      for (int j = 0; j < 64; ++j)
-        if (j < L) mx = fmaxf(mx, __uint_as_float(s[j]));
-      const float mxs = mx * scale_log2;
+        for (int j = 0; j < 64; j += 2) {
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&addh[j >> 1]));
+          const float t0 = fmaf(__uint_as_float(s[j]), scale_log2, a.x);
+          const float t1 = fmaf(__uint_as_float(s[j + 1]), scale_log2, a.y);
+          s[j] = __float_as_uint(t0);
+          s[j + 1] = __float_as_uint(t1);
+          if (j < L) mx = fmaxf(mx, t0);
+          if (j + 1 < L) mx = fmaxf(mx, t1);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (j < L) mx = fmaxf(mx, __uint_as_float(s[j]));
+      }
+      const float mxs = ADD ? mx : mx * scale_log2;
+      const float sl2 = ADD ? 1.f : scale_log2;
       float sum = 0.f;
 #pragma unroll
       for (int j = 0; j < 64; ++j) {
-        const float p = j < L ? ex2(fmaf(__uint_as_float(s[j]), scale_log2, -mxs)) : 0.f;
+        const float p = j < L ? ex2(fmaf(__uint_as_float(s[j]), sl2, -mxs)) : 0.f;
         s[j] = __float_as_uint(p);
         sum += p;
       }
@@ -262,22 +332,37 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->p_ready);
-      // dS = scale * P * (dP - rho)  (keys >= L forced to exactly 0)
-      const float srho = scale * rho;
+      // dS = scale * P * (dP - rho)  (keys >= L forced to exactly 0); dBias += P (dP - rho)
       uint8_t* dsrow = sDS + prow_off;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t w[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int j = 8 * c + 2 * t;
-          const float a = __uint_as_float(s[j]) * fmaf(__uint_as_float(dp[j]), scale, -srho);
-          const float b = __uint_as_float(s[j + 1]) * fmaf(__uint_as_float(dp[j + 1]), scale, -srho);
-          w[t] = pack2<T>(j < L ? a : 0.f, j + 1 < L ? b : 0.f);
+      for (int g = 0; g < 4; ++g) {
+        if (LK > 0 && g * 16 >= LK) break;
+        uint32_t acc[16];
+        if constexpr (DBIAS) {
+          tmem_ld16(tmem + t_lane + C::kTdB + g * 16, *reinterpret_cast<uint32_t(*)[16]>(acc));
+          tmem_wait_ld();
         }
-        if (c < p_chunks)
-          *reinterpret_cast<uint4*>(dsrow + ((c ^ pswz) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = 2 * g + h2;
+          uint32_t w[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int j = 8 * c + 2 * t;
+            const float a = j < L ? __uint_as_float(s[j]) * (__uint_as_float(dp[j]) - rho) : 0.f;
+            const float b = j + 1 < L ? __uint_as_float(s[j + 1]) * (__uint_as_float(dp[j + 1]) - rho) : 0.f;
+            if constexpr (DBIAS) {
+              acc[8 * h2 + 2 * t] = __float_as_uint(__uint_as_float(acc[8 * h2 + 2 * t]) + a);
+              acc[8 * h2 + 2 * t + 1] = __float_as_uint(__uint_as_float(acc[8 * h2 + 2 * t + 1]) + b);
+            }
+            w[t] = pack2<T>(a * scale, b * scale);
+          }
+          if (c < p_chunks)
+            *reinterpret_cast<uint4*>(dsrow + ((c ^ pswz) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        if constexpr (DBIAS) tmem_st16(tmem + t_lane + C::kTdB + g * 16, acc);
       }
+      if constexpr (DBIAS) tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->ds_ready);
@@ -315,6 +400,21 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         mbar_arrive(&bars->empty[st]);   // stage may be refilled
       }
     }
+    if constexpr (DBIAS) {
+      // this CTA's dS partials: ws[cta][row][0..63] (reduced per head in fixed order later)
+      float* wrow = add.dbias_ws + ((size_t)blockIdx.x * kTileRows + row) * 64;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint32_t acc[16];
+        tmem_ld16(tmem + t_lane + C::kTdB + g * 16, *reinterpret_cast<uint32_t(*)[16]>(acc));
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 16; t += 4)
+          *reinterpret_cast<float4*>(wrow + g * 16 + t) =
+              make_float4(__uint_as_float(acc[t]), __uint_as_float(acc[t + 1]),
+                          __uint_as_float(acc[t + 2]), __uint_as_float(acc[t + 3]));
+      }
+    }
     if (leader) bulk_wait<0>();
   }
   tc_fence_before();
@@ -323,15 +423,53 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
 }
 
-template <typename T, int D, int LK>
+// dbias[h][i][j] = sum over CTAs c (ascending) and slots u with (2c+u) % heads == h of
+// ws[c][64u + i][j]  — fixed order, deterministic.
+__global__ void dbias_tc_reduce_kernel(const float* __restrict__ ws, int grid, int heads, int L,
+                                       float* __restrict__ dbias) {
+  const int n = heads * L * L;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int h = e / (L * L);
+    const int r = e - h * L * L;
+    const int i = r / L, j = r % L;
+    float acc = 0.f;
+    for (int c = 0; c < grid; ++c) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if ((2 * c + u) % heads == h) acc += ws[((size_t)c * kTileRows + 64 * u + i) * 64 + j];
+    }
+    dbias[e] = acc;
+  }
+}
+
+int bwd_period_tiles(const Geom& g, bool period_bias, bool has_mask) {
+  if (!period_bias && !has_mask) return 1;
+  const int64_t pu = (int64_t)g.heads * (has_mask ? g.mask_windows : 1);
+  const int64_t pt = (pu % 2 == 0) ? pu / 2 : pu;
+  return pt > (1 << 30) ? (1 << 30) : (int)pt;
+}
+
+template <int D>
+int bwd_grid(const Geom& g, bool period_bias, bool has_mask) {
+  const int n_tiles = (int)((g.units + 1) / 2);
+  int grid = std::max(1, std::min(n_tiles, device_sm_count() * BCfg<D>::kCtasPerSm));
+  if ((period_bias || has_mask) && n_tiles > grid) {
+    const int pt = bwd_period_tiles(g, period_bias, has_mask);
+    grid = (grid / pt) * pt;
+  }
+  return grid;
+}
+
+template <typename T, int D, int LK, bool ADD, bool DBIAS>
 int launch_bwd_t(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                 const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
+                 const void* dout, const float* bias, const float* mask, void* dq, void* dk,
+                 void* dv, float* dbias, float* ws, cudaStream_t s) {
   CUtensorMap m[7];
   const void* ptrs[7] = {q, k, v, dout, dq, dk, dv};
   int rc;
   for (int i = 0; i < 7; ++i)
     if ((rc = get_units_map(&m[i], ptrs[i], dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
-  auto kern = bwd_tc_kernel<T, D, LK>;
+  auto kern = bwd_tc_kernel<T, D, LK, ADD, DBIAS>;
   constexpr int smem = BCfg<D>::kSmem;
   static bool attr_done = false;
   if (!attr_done) {
@@ -341,52 +479,98 @@ int launch_bwd_t(const Geom& g, int dtype, const void* q, const void* k, const v
     attr_done = true;
   }
   const int n_tiles = (int)((g.units + 1) / 2);
-  const int grid = std::max(1, std::min(n_tiles, device_sm_count() * BCfg<D>::kCtasPerSm));
+  const int grid = bwd_grid<D>(g, ADD || DBIAS, mask != nullptr);
+  BwdAddArgs add{bias, mask, ws, g.heads, mask ? g.mask_windows : 1};
   rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, m[0], m[1], m[2], m[3],
-                             m[4], m[5], m[6], n_tiles, (int)g.L, g.scale, device_flags_ptr()),
+                             m[4], m[5], m[6], n_tiles, (int)g.L, g.scale, add,
+                             device_flags_ptr()),
                   "bwd_tc_kernel launch");
   if (rc) return rc;
   count_launch();
-  return FWA_OK;
+  if (DBIAS) {
+    const int n = g.heads * g.L * g.L;
+    dbias_tc_reduce_kernel<<<std::max(1, std::min((n + 255) / 256, 1024)), 256, 0, s>>>(
+        ws, grid, g.heads, g.L, dbias);
+    count_launch();
+    rc = check_cuda(cudaGetLastError(), "dbias_tc_reduce_kernel launch");
+  }
+  return rc;
+}
+
+template <typename T, int D, int LK>
+int bwd_dispatch_flags(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                       const void* dout, const float* b, const float* m, void* dq, void* dk,
+                       void* dv, float* db, float* ws, cudaStream_t s) {
+  const bool add = b || m;
+  if (db) {
+    return add ? launch_bwd_t<T, D, LK, true, true>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s)
+               : launch_bwd_t<T, D, LK, false, true>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
+  }
+  return add ? launch_bwd_t<T, D, LK, true, false>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s)
+             : launch_bwd_t<T, D, LK, false, false>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
 }
 
 template <typename T, int D>
 int bwd_dispatch_l(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                   const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
-  if (g.L == 49) return launch_bwd_t<T, D, 49>(g, dtype, q, k, v, dout, dq, dk, dv, s);
-  if (g.L == 64) return launch_bwd_t<T, D, 64>(g, dtype, q, k, v, dout, dq, dk, dv, s);
-  return launch_bwd_t<T, D, 0>(g, dtype, q, k, v, dout, dq, dk, dv, s);
+                   const void* dout, const float* b, const float* m, void* dq, void* dk, void* dv,
+                   float* db, float* ws, cudaStream_t s) {
+  if (g.L == 49) return bwd_dispatch_flags<T, D, 49>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
+  if (g.L == 64) return bwd_dispatch_flags<T, D, 64>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
+  return bwd_dispatch_flags<T, D, 0>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
 }
 
 template <typename T>
 int bwd_dispatch_d(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                   const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
+                   const void* dout, const float* b, const float* m, void* dq, void* dk, void* dv,
+                   float* db, float* ws, cudaStream_t s) {
   switch (g.d) {
-    case 16: return bwd_dispatch_l<T, 16>(g, dtype, q, k, v, dout, dq, dk, dv, s);
-    case 32: return bwd_dispatch_l<T, 32>(g, dtype, q, k, v, dout, dq, dk, dv, s);
-    case 64: return bwd_dispatch_l<T, 64>(g, dtype, q, k, v, dout, dq, dk, dv, s);
+    case 16: return bwd_dispatch_l<T, 16>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
+    case 32: return bwd_dispatch_l<T, 32>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
+    case 64: return bwd_dispatch_l<T, 64>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
   }
   return fail(FWA_ERR_CAPACITY, "tcgen05 backward: unsupported head_dim");
 }
 
 }  // namespace
 
-bool tc_bwd_supported(const Geom& g, int dtype, bool bias_or_mask) {
-  if (bias_or_mask) return false;
+bool tc_bwd_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias) {
   if (dtype != FWA_F16 && dtype != FWA_BF16) return false;
   if (g.L < 1 || g.L > kUnitRows) return false;
   if (g.d != 16 && g.d != 32 && g.d != 64) return false;
-  return g.units <= ((int64_t)1 << 31);
+  if (g.units > ((int64_t)1 << 31)) return false;
+  if (has_bias || has_mask || want_dbias) {
+    const int64_t n_tiles = (g.units + 1) / 2;
+    const int cap = device_sm_count() * (g.d <= 32 ? 2 : 1);
+    if (n_tiles > cap && bwd_period_tiles(g, has_bias || want_dbias, has_mask) > cap) return false;
+  }
+  return true;
 }
 
 size_t tc_bwd_smem(const Geom& g) {
   return g.d == 16 ? BCfg<16>::kSmem : g.d == 32 ? BCfg<32>::kSmem : BCfg<64>::kSmem;
 }
 
+int tc_bwd_tmem_cols(const Geom& g) {
+  return g.d == 16 ? BCfg<16>::kTmemCols : g.d == 32 ? BCfg<32>::kTmemCols : BCfg<64>::kTmemCols;
+}
+
+size_t tc_bwd_workspace_bytes(const Geom& g, bool has_mask, bool want_dbias) {
+  if (!want_dbias) return 0;
+  int grid = 1;
+  switch (g.d) {
+    case 16: grid = bwd_grid<16>(g, true, has_mask); break;
+    case 32: grid = bwd_grid<32>(g, true, has_mask); break;
+    default: grid = bwd_grid<64>(g, true, has_mask); break;
+  }
+  return (size_t)grid * kTileRows * 64 * sizeof(float);
+}
+
 int launch_bwd_tc(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                  const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
-  return dtype == FWA_BF16 ? bwd_dispatch_d<__nv_bfloat16>(g, dtype, q, k, v, dout, dq, dk, dv, s)
-                           : bwd_dispatch_d<__half>(g, dtype, q, k, v, dout, dq, dk, dv, s);
+                  const void* dout, const float* bias, const float* mask, void* dq, void* dk,
+                  void* dv, float* dbias, float* ws, cudaStream_t s) {
+  return dtype == FWA_BF16
+             ? bwd_dispatch_d<__nv_bfloat16>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s)
+             : bwd_dispatch_d<__half>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
 }
 
 }  // namespace fwa

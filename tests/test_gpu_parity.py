@@ -317,6 +317,40 @@ def test_forward_bias_mask_full_size(dt, N, h, L, d, nW, use_bias):
     assert fwa._native.device_flags() == 0
 
 
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("N,h,L,d,nW,use_bias,want_db", [
+    (8192, 3, 49, 32, 64, True, True),    # Swin-T stage 1 shifted layer, learnable bias
+    (512, 12, 49, 32, 4, True, True),
+    (128, 24, 49, 32, 0, True, True),
+    (3000, 5, 49, 16, 7, True, False),
+    (1500, 3, 64, 64, 0, True, True),
+    (999, 2, 36, 32, 9, False, False),
+    (600, 1, 49, 32, 300, True, True),    # period above the grid cap -> generic kernel
+])
+def test_backward_bias_mask_full_size(dt, N, h, L, d, nW, use_bias, want_db):
+    dtype = DTYPES[dt]
+    rng = fwa.Rng(N + 2 * h)
+    q, k, v, do = (fwa.fill_uniform(rng, (N, h, L, d), dtype=dtype) for _ in range(4))
+    bias = fwa.fill_uniform(rng, (h, L, L), -1.0, 1.0) if use_bias else None
+    mask = None
+    if nW:
+        mask = torch.where(fwa.fill_uniform(rng, (nW, L, L)) > 0.4, -100.0, 0.0).float().contiguous()
+    sc = d ** -0.5
+    dq, dk, dv, db = ops.attention_backward(q, k, v, do, sc, bias, mask, want_dbias=want_db)
+    qf, kf, vf = (t.float().requires_grad_() for t in (q, k, v))
+    bf = bias.clone().requires_grad_() if bias is not None else None
+    ref = _torch_ref(qf, kf, vf, sc, bf, mask)
+    ref.backward(do.float())
+    for got, t in ((dq, qf), (dk, kf), (dv, vf)):
+        assert (got.float() - t.grad).abs().max().item() <= 2e-2
+    if want_db:
+        scale_db = max(1.0, bf.grad.abs().max().item())
+        assert (db - bf.grad).abs().max().item() <= 1e-2 * scale_db
+        _, _, _, db2 = ops.attention_backward(q, k, v, do, sc, bias, mask, want_dbias=True)
+        assert torch.equal(db, db2)  # deterministic
+    assert fwa._native.device_flags() == 0
+
+
 def test_footprint_reports_kernel_and_paper_peaks():
     fp = ops.footprint(8192, 3, 49, 32, torch.float16, chunks=2)
     assert fp["paper_peak_fwd"] == (49 * 49 + 2 * 49 * 16) * 2
