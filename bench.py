@@ -200,10 +200,13 @@ def run_gpu(args, wl):
         if wl["extras"]:
             table = fwa.fill_uniform(rng, ((2 * k - 1) ** 2, h), -0.04, 0.04, device=dev)
             bias = ops.bias_gather(table, k)
-            # shifted layers (odd index within a stage) use the mask; stage 4 (7x7) has no shift
+            # Swin alternates W-MSA / SW-MSA: the second block of each pair is shifted and
+            # masked; the last stage (7x7 map = one window) never shifts.
             nW = N // wl["batch"]
             side = int(round(math.sqrt(nW))) * k
-            mask = ops.shift_mask(side, side, k, k // 2, device=dev) if nW > 1 else None
+            idx_in_stage = sum(1 for x in layers[:len(bufs)] if x == (N, h, L, d))
+            if nW > 1 and idx_in_stage % 2 == 1:
+                mask = ops.shift_mask(side, side, k, k // 2, device=dev)
         o = torch.empty_like(q)
         bufs.append((q, kk, v, do, bias, mask, o, d ** -0.5))
     torch.cuda.synchronize()

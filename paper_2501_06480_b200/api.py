@@ -21,6 +21,7 @@ import numpy as np
 import torch
 
 from . import ops
+from .pipeline import host_backward, host_forward
 from .errors import CapacityError, ContextError, FlashwinError, InvalidRangeError, ShapeError
 from .tiling import (
     FlashContext,
@@ -100,6 +101,32 @@ def _to_device(x, dtype: Optional[torch.dtype] = None, device=None):
             else torch.float32
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     return src.to(device=dev, dtype=dtype, non_blocking=False).contiguous(), kind, host_dtype
+
+
+def _to_host_tensor(x, dtype: Optional[torch.dtype] = None):
+    """Host torch tensor in a kernel dtype (f16/bf16/f32) + (kind, host dtype) to convert back."""
+    if isinstance(x, torch.Tensor):
+        kind, host_dtype, t = _Kind.TORCH_CPU, x.dtype, x
+    else:
+        kind = _Kind.DENSE if hasattr(x, "array") else _Kind.NUMPY
+        arr = np.asarray(x.array if kind == _Kind.DENSE else x)
+        host_dtype, t = arr.dtype, torch.from_numpy(np.ascontiguousarray(arr))
+    if dtype is None:
+        dtype = t.dtype if t.dtype in (torch.float16, torch.bfloat16, torch.float32) else torch.float32
+    return t.to(dtype).contiguous(), kind, host_dtype
+
+
+def _from_host(t: torch.Tensor, kind, host_dtype):
+    if kind == _Kind.TORCH_CPU:
+        return t if t.dtype == host_dtype else t.to(host_dtype)
+    a = t.to(torch.float64).numpy()
+    if kind == _Kind.DENSE:
+        return HostArray(a)
+    return a.astype(host_dtype, copy=False)
+
+
+def _is_device(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
 
 
 def _from_device(t: torch.Tensor, kind, host_dtype):
@@ -220,15 +247,24 @@ def batched_flash_forward(q, k, v, cfg: TileConfig, arenas: Sequence[ScratchpadA
         arenas[0].check("forward", need)
     except FlashwinError as exc:
         raise type(exc)(f"slice (b=0, head=0): {exc}") from exc
-    qd, kind, hdt = _to_device(q)
-    kd, _, _ = _to_device(k, qd.dtype, qd.device)
-    vd, _, _ = _to_device(v, qd.dtype, qd.device)
-    o = ops.attention_forward(qd, kd, vd, cfg.scale, bias, mask, chunks=cfg.r, kernel=kernel)
+    if _is_device(q):
+        qd, kind, hdt = _to_device(q)
+        kd, _, _ = _to_device(k, qd.dtype, qd.device)
+        vd, _, _ = _to_device(v, qd.dtype, qd.device)
+        o = ops.attention_forward(qd, kd, vd, cfg.scale, bias, mask, chunks=cfg.r, kernel=kernel)
+        result = _from_device(o, kind, hdt)
+    else:
+        # host buffers: chunked H2D / kernel / D2H overlap (pipeline.py)
+        qh, kind, hdt = _to_host_tensor(q)
+        kh, _, _ = _to_host_tensor(k, qh.dtype)
+        vh, _, _ = _to_host_tensor(v, qh.dtype)
+        result = _from_host(host_forward(qh, kh, vh, cfg.scale, bias, mask, cfg.r, kernel),
+                            kind, hdt)
     for a in arenas[: min(len(arenas), B * h)]:
         a.record(need)
     report = forward_report(B * h, L, C, max(a.peak_bytes for a in arenas[: min(len(arenas), B * h)]))
     ctxs = BatchedContexts(q, k, v, cfg, bias, mask)
-    return _from_device(o, kind, hdt), ctxs, report
+    return result, ctxs, report
 
 
 def batched_flash_backward(contexts: BatchedContexts, dO, arenas: Sequence[ScratchpadArena], *,
@@ -251,17 +287,24 @@ def batched_flash_backward(contexts: BatchedContexts, dO, arenas: Sequence[Scrat
         arenas[0].check("backward", need)
     except FlashwinError as exc:
         raise type(exc)(f"slice (b=0, head=0): {exc}") from exc
-    dod, kind, hdt = _to_device(dO)
-    qd, _, _ = _to_device(contexts.q, dod.dtype, dod.device)
-    kd, _, _ = _to_device(contexts.k, dod.dtype, dod.device)
-    vd, _, _ = _to_device(contexts.v, dod.dtype, dod.device)
-    dq, dk, dv, db = ops.attention_backward(qd, kd, vd, dod, cfg.scale, contexts.bias,
-                                            contexts.mask, chunks=cfg.r, kernel=kernel,
-                                            want_dbias=want_dbias)
+    if _is_device(dO):
+        dod, kind, hdt = _to_device(dO)
+        qd, _, _ = _to_device(contexts.q, dod.dtype, dod.device)
+        kd, _, _ = _to_device(contexts.k, dod.dtype, dod.device)
+        vd, _, _ = _to_device(contexts.v, dod.dtype, dod.device)
+        dq, dk, dv, db = ops.attention_backward(qd, kd, vd, dod, cfg.scale, contexts.bias,
+                                                contexts.mask, chunks=cfg.r, kernel=kernel,
+                                                want_dbias=want_dbias)
+        out = [_from_device(t, kind, hdt) for t in (dq, dk, dv)]
+    else:
+        doh, kind, hdt = _to_host_tensor(dO)
+        qh, kh, vh = (_to_host_tensor(t, doh.dtype)[0] for t in (contexts.q, contexts.k, contexts.v))
+        dq, dk, dv, db = host_backward(qh, kh, vh, doh, cfg.scale, contexts.bias, contexts.mask,
+                                       cfg.r, kernel, want_dbias)
+        out = [_from_host(t, kind, hdt) for t in (dq, dk, dv)]
     for a in arenas[: min(len(arenas), B * h)]:
         a.record(need)
     report = backward_report(B * h, L, C, max(a.peak_bytes for a in arenas[: min(len(arenas), B * h)]))
-    out = [_from_device(t, kind, hdt) for t in (dq, dk, dv)]
     if want_dbias:
         out.append(db)
     return (*out, report)

@@ -51,7 +51,8 @@ struct BCfg {
   static constexpr int kStages = D <= 16 ? 4 : 2;
   static constexpr int kCtasPerSm = D <= 32 ? 2 : 1;
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
-  static constexpr int kSmem = kStages * kStageBytes + 2 * kPBytes + 256;
+  // + 16 KB: the CTA's (bias + mask) * log2e rows as f16 (ADD variants)
+  static constexpr int kSmem = kStages * kStageBytes + 3 * kPBytes + 256;
   static constexpr int kChunks = kRowBytes / 16;
   // TMEM (lane = tile row): S [0,64) | dP [64,128) | dBias acc [128,192) |
   // gradients dV, dK, dQ at [0,3d) when they fit in the S/dP columns, else [192,192+3d).
@@ -101,7 +102,8 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   uint8_t* sStage = smem;                                  // [stage][Q|K|V|dO]
   uint8_t* sP = smem + C::kStages * C::kStageBytes;
   uint8_t* sDS = sP + kPBytes;
-  BwdBarriers* bars = reinterpret_cast<BwdBarriers*>(sDS + kPBytes);
+  uint8_t* sAdd = sDS + kPBytes;  // [128 rows][64] f16, SW128-style chunk swizzle
+  BwdBarriers* bars = reinterpret_cast<BwdBarriers*>(sAdd + kPBytes);
   auto slot = [&](int st, int which) { return sStage + st * C::kStageBytes + which * C::kTileBytes; };
   // The swizzled layouts need a 1024-byte aligned base; the budget leaves no slack
   // for manual alignment (2 CTAs/SM), so verify it and report instead of computing garbage.
@@ -242,7 +244,7 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
     const bool leader = (threadIdx.x == 64);
     const int p_chunks = LK > 0 ? (LK + 7) / 8 : 8;
     const float scale_log2 = scale * 1.4426950408889634f;
-    uint32_t addh[ADD ? 32 : 1];
+    uint8_t* arow = sAdd + prow_off;
     if constexpr (ADD) {
       const int u0 = 2 * (int)blockIdx.x + ul;  // same (w, h) for every tile of this CTA
       const int hd = u0 % add.heads;
@@ -250,14 +252,20 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
       const float* brow = add.bias ? add.bias + ((size_t)hd * L + r_in) * L : nullptr;
       const float* mrow = add.mask ? add.mask + ((size_t)w * L + r_in) * L : nullptr;
 #pragma unroll
-      for (int j = 0; j < 64; j += 2) {
-        float a = 0.f, b = 0.f;
-        if (r_in < L) {
-          if (j < L) a = ((brow ? brow[j] : 0.f) + (mrow ? mrow[j] : 0.f)) * 1.4426950408889634f;
-          if (j + 1 < L) b = ((brow ? brow[j + 1] : 0.f) + (mrow ? mrow[j + 1] : 0.f)) * 1.4426950408889634f;
+      for (int c = 0; c < 8; ++c) {
+        uint32_t wv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int j = 8 * c + 2 * t;
+          float a = 0.f, b = 0.f;
+          if (r_in < L) {
+            if (j < L) a = ((brow ? brow[j] : 0.f) + (mrow ? mrow[j] : 0.f)) * 1.4426950408889634f;
+            if (j + 1 < L) b = ((brow ? brow[j + 1] : 0.f) + (mrow ? mrow[j + 1] : 0.f)) * 1.4426950408889634f;
+          }
+          __half2 h2 = __floats2half2_rn(a, b);
+          wv[t] = *reinterpret_cast<uint32_t*>(&h2);
         }
-        __half2 h2 = __floats2half2_rn(a, b);
-        addh[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+        *reinterpret_cast<uint4*>(arow + ((c ^ pswz) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       }
     }
     if constexpr (DBIAS) {
@@ -286,14 +294,21 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
       float mx = -INFINITY;
       if constexpr (ADD) {
 #pragma unroll
-        for (int j = 0; j < 64; j += 2) {
-          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&addh[j >> 1]));
-          const float t0 = fmaf(__uint_as_float(s[j]), scale_log2, a.x);
-          const float t1 = fmaf(__uint_as_float(s[j + 1]), scale_log2, a.y);
-          s[j] = __float_as_uint(t0);
-          s[j + 1] = __float_as_uint(t1);
-          if (j < L) mx = fmaxf(mx, t0);
-          if (j + 1 < L) mx = fmaxf(mx, t1);
+        for (int c = 0; c < 8; ++c) {
+          if (LK > 0 && 8 * c >= LK) break;
+          const uint4 av = *reinterpret_cast<const uint4*>(arow + ((c ^ pswz) << 4));
+          const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int j = 8 * c + 2 * t;
+            const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&aw[t]));
+            const float t0 = fmaf(__uint_as_float(s[j]), scale_log2, a.x);
+            const float t1 = fmaf(__uint_as_float(s[j + 1]), scale_log2, a.y);
+            s[j] = __float_as_uint(t0);
+            s[j + 1] = __float_as_uint(t1);
+            if (j < L) mx = fmaxf(mx, t0);
+            if (j + 1 < L) mx = fmaxf(mx, t1);
+          }
         }
       } else {
 #pragma unroll
@@ -423,22 +438,27 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
 }
 
-// dbias[h][i][j] = sum over CTAs c (ascending) and slots u with (2c+u) % heads == h of
-// ws[c][64u + i][j]  — fixed order, deterministic.
+// dbias[h][i][j] = sum over (CTA c, slot u) with (2c+u) % heads == h of ws[c][64u + i][j].
+// One warp per element: lane l sums c = l, l+32, ... in order, then a fixed shuffle tree —
+// the same order every run (deterministic, no atomics).
 __global__ void dbias_tc_reduce_kernel(const float* __restrict__ ws, int grid, int heads, int L,
                                        float* __restrict__ dbias) {
   const int n = heads * L * L;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n; e += warps) {
     const int h = e / (L * L);
     const int r = e - h * L * L;
     const int i = r / L, j = r % L;
     float acc = 0.f;
-    for (int c = 0; c < grid; ++c) {
+    for (int c = lane; c < grid; c += 32) {
 #pragma unroll
       for (int u = 0; u < 2; ++u)
         if ((2 * c + u) % heads == h) acc += ws[((size_t)c * kTileRows + 64 * u + i) * 64 + j];
     }
-    dbias[e] = acc;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) dbias[e] = acc;
   }
 }
 
@@ -489,7 +509,7 @@ int launch_bwd_t(const Geom& g, int dtype, const void* q, const void* k, const v
   count_launch();
   if (DBIAS) {
     const int n = g.heads * g.L * g.L;
-    dbias_tc_reduce_kernel<<<std::max(1, std::min((n + 255) / 256, 1024)), 256, 0, s>>>(
+    dbias_tc_reduce_kernel<<<std::max(1, std::min((n * 32 + 255) / 256, 4096)), 256, 0, s>>>(
         ws, grid, g.heads, g.L, dbias);
     count_launch();
     rc = check_cuda(cudaGetLastError(), "dbias_tc_reduce_kernel launch");
