@@ -105,14 +105,16 @@ int validate(const fwa_desc* d, Geom* g, bool need_mask_windows_if_mask, const f
 
 int pick_fwd(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask, int* kernel,
              size_t* smem, int* tmem) {
-  const bool tc_ok = tc_fwd_supported(g, d->dtype, has_bias, has_mask);
+  const bool tc_small = tc_fwd_supported(g, d->dtype, has_bias, has_mask);
+  const bool tc_large = !tc_small && tc_fwd_large_supported(g, d->dtype, has_bias, has_mask);
+  const bool tc_ok = tc_small || tc_large;
   if (d->kernel == FWA_KERNEL_TC && !tc_ok)
     return fail(FWA_ERR_CAPACITY, "tcgen05 forward does not support this shape/dtype (L=" +
                                       std::to_string(g.L) + ", d=" + std::to_string(g.d) + ")");
   if (tc_ok && d->kernel != FWA_KERNEL_GENERIC) {
     *kernel = FWA_KERNEL_TC;
-    *smem = tc_fwd_smem(g, d->dtype);
-    *tmem = tc_fwd_tmem_cols(g);
+    *smem = tc_small ? tc_fwd_smem(g, d->dtype) : tc_fwd_large_smem(g);
+    *tmem = tc_small ? tc_fwd_tmem_cols(g) : 256;
     return FWA_OK;
   }
   *kernel = FWA_KERNEL_GENERIC;
@@ -218,7 +220,11 @@ extern "C" int fwa_fwd(const fwa_desc* desc, const void* q, const void* k, const
   rc = pick_fwd(desc, g, bias != nullptr, mask != nullptr, &kern, &smem, &tmem);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (kern == FWA_KERNEL_TC) return launch_fwd_tc(g, desc->dtype, q, k, v, bias, mask, o, s);
+  if (kern == FWA_KERNEL_TC) {
+    if (tc_fwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr))
+      return launch_fwd_tc(g, desc->dtype, q, k, v, bias, mask, o, s);
+    return launch_fwd_tc_large(g, desc->dtype, q, k, v, o, s);
+  }
   return launch_fwd_generic(g, desc->dtype, q, k, v, bias, mask, o, s);
 }
 

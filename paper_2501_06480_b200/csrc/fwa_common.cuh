@@ -98,6 +98,12 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// tcgen05 / TMA forward for 64 < L <= 256 (fwa_tc_fwd_large.cu)
+bool tc_fwd_large_supported(const Geom& g, int dtype, bool has_bias, bool has_mask);
+size_t tc_fwd_large_smem(const Geom& g);
+int launch_fwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                        void* o, cudaStream_t s);
+
 // tcgen05 / TMA backward (fwa_tc_bwd.cu)
 bool tc_bwd_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias);
 size_t tc_bwd_smem(const Geom& g);

@@ -246,27 +246,27 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
     const float scale_log2 = scale * 1.4426950408889634f;
     uint8_t* arow = sAdd + prow_off;
     if constexpr (ADD) {
-      const int u0 = 2 * (int)blockIdx.x + ul;  // same (w, h) for every tile of this CTA
-      const int hd = u0 % add.heads;
-      const int w = (u0 / add.heads) % add.mask_windows;
-      const float* brow = add.bias ? add.bias + ((size_t)hd * L + r_in) * L : nullptr;
-      const float* mrow = add.mask ? add.mask + ((size_t)w * L + r_in) * L : nullptr;
+      // Cooperative, coalesced fill of the CTA's two (bias + mask) * log2e tiles
+      // (every tile of this CTA has the same (w, h) pair per slot): f16, swizzled rows.
+      const int ct = threadIdx.x - 64;             // 0..127 within the softmax warps
+      for (int i = ct; i < 2 * 64 * 64 / 2; i += 128)
+        reinterpret_cast<uint32_t*>(sAdd)[i] = 0u;
+      named_sync(3, 128);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t wv[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int j = 8 * c + 2 * t;
-          float a = 0.f, b = 0.f;
-          if (r_in < L) {
-            if (j < L) a = ((brow ? brow[j] : 0.f) + (mrow ? mrow[j] : 0.f)) * 1.4426950408889634f;
-            if (j + 1 < L) b = ((brow ? brow[j + 1] : 0.f) + (mrow ? mrow[j + 1] : 0.f)) * 1.4426950408889634f;
-          }
-          __half2 h2 = __floats2half2_rn(a, b);
-          wv[t] = *reinterpret_cast<uint32_t*>(&h2);
+      for (int u = 0; u < 2; ++u) {
+        const int uu = 2 * (int)blockIdx.x + u;
+        const int hd = uu % add.heads;
+        const int w = (uu / add.heads) % add.mask_windows;
+        const float* __restrict__ bt = add.bias ? add.bias + (size_t)hd * L * L : nullptr;
+        const float* __restrict__ mt = add.mask ? add.mask + (size_t)w * L * L : nullptr;
+        for (int e = ct; e < L * L; e += 128) {
+          const float a = ((bt ? __ldg(bt + e) : 0.f) + (mt ? __ldg(mt + e) : 0.f)) * 1.4426950408889634f;
+          const int r = u * 64 + e / L, j = e % L;
+          uint8_t* dst = sAdd + (r >> 3) * 1024 + (r & 7) * 128 + ((((j >> 3) ^ (r & 7))) << 4) + (j & 7) * 2;
+          *reinterpret_cast<__half*>(dst) = __float2half_rn(a);
         }
-        *reinterpret_cast<uint4*>(arow + ((c ^ pswz) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       }
+      named_sync(3, 128);
     }
     if constexpr (DBIAS) {
       uint32_t z[16];

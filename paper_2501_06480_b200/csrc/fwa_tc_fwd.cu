@@ -50,15 +50,17 @@ constexpr int kThreads = 192;
 constexpr int kTileRows = 128;     // MMA M
 constexpr int kUnitRows = 64;      // rows per packed unit
 
-template <int D>
+template <int D, bool ADD = false>
 struct Cfg {
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTileBytes = kTileRows * kRowBytes;            // one of Q/K/V per stage
-  static constexpr int kStages = D <= 16 ? 8 : 4;
+  // with bias/mask, 16 KB of smem hold the CTA's (bias + mask) rows: one stage fewer
+  static constexpr int kStages = D <= 16 ? (ADD ? 6 : 8) : (ADD ? 3 : 4);
+  static constexpr int kAddBytes = ADD ? 128 * 128 : 0;
   static constexpr int kCtasPerSm = D <= 32 ? 2 : 1;
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);  // UMMA layout code
   static constexpr int kSmem = 1024 /*align slack*/ + kStages * 3 * kTileBytes +
-                               kTileBytes /*O staging*/ + 256 /*barriers*/;
+                               kTileBytes /*O staging*/ + kAddBytes + 256 /*barriers*/;
   static constexpr int kChunks = kRowBytes / 16;  // 16-byte chunks per row
   // TMEM columns (lane = tile row; unit 0 rows are lanes 0-63, unit 1 rows 64-127):
   //   S [0,64) fp32 | P [64,96) 16-bit pairs | O0, O1 (d each) fp32.
@@ -88,11 +90,11 @@ struct AddArgs {
 
 // LK > 0: compile-time window length (Swin 7x7 / 8x8); LK == 0: runtime L.
 template <typename T, int D, int LK, bool ADD>
-__global__ void __launch_bounds__(kThreads, Cfg<D>::kCtasPerSm)
+__global__ void __launch_bounds__(kThreads, Cfg<D, ADD>::kCtasPerSm)
 fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
               int n_tiles, int L_rt, float scale_log2, AddArgs add) {
-  using C = Cfg<D>;
+  using C = Cfg<D, ADD>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   const int L = LK > 0 ? LK : L_rt;
   extern __shared__ uint8_t smem_raw[];
@@ -102,7 +104,8 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   uint8_t* sK = sQ + C::kStages * C::kTileBytes;
   uint8_t* sV = sK + C::kStages * C::kTileBytes;
   uint8_t* sO = sV + C::kStages * C::kTileBytes;   // 1 staging tile for the TMA store
-  SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(sO + C::kTileBytes);
+  uint8_t* sAdd = sO + C::kTileBytes;              // [128 rows][64] f16 add rows (ADD)
+  SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(sAdd + C::kAddBytes);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -218,24 +221,30 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
     uint8_t* orow = sO + row * C::kRowBytes;
     const uint32_t oswz = (uint32_t)((row * C::kRowBytes) >> 7) & (C::kChunks - 1);
     const bool leader = (threadIdx.x == 64);
-    uint32_t addh[ADD ? 32 : 1];
+    const uint32_t aswz = (uint32_t)(row & 7);
+    uint8_t* arow = sAdd + (row >> 3) * 1024 + (row & 7) * 128;
     if constexpr (ADD) {
-      const int r_in = row & 63;
-      const int u0 = 2 * (int)blockIdx.x + ul;  // same (w, h) for every tile of this CTA
-      const int hd = u0 % add.heads;
-      const int w = (u0 / add.heads) % add.mask_windows;
-      const float* brow = add.bias ? add.bias + ((size_t)hd * L + r_in) * L : nullptr;
-      const float* mrow = add.mask ? add.mask + ((size_t)w * L + r_in) * L : nullptr;
+      // Cooperative, coalesced fill of the CTA's two (bias + mask) * log2e tiles
+      // (every tile of this CTA has the same (w, h) pair per slot): f16, swizzled rows.
+      const int ct = threadIdx.x - 64;             // 0..127 within the softmax warps
+      for (int i = ct; i < 2 * 64 * 64 / 2; i += 128)
+        reinterpret_cast<uint32_t*>(sAdd)[i] = 0u;
+      named_sync(3, 128);
 #pragma unroll
-      for (int j = 0; j < 64; j += 2) {
-        float a = 0.f, b = 0.f;
-        if (r_in < L) {
-          if (j < L) a = ((brow ? brow[j] : 0.f) + (mrow ? mrow[j] : 0.f)) * 1.4426950408889634f;
-          if (j + 1 < L) b = ((brow ? brow[j + 1] : 0.f) + (mrow ? mrow[j + 1] : 0.f)) * 1.4426950408889634f;
+      for (int u = 0; u < 2; ++u) {
+        const int uu = 2 * (int)blockIdx.x + u;
+        const int hd = uu % add.heads;
+        const int w = (uu / add.heads) % add.mask_windows;
+        const float* __restrict__ bt = add.bias ? add.bias + (size_t)hd * L * L : nullptr;
+        const float* __restrict__ mt = add.mask ? add.mask + (size_t)w * L * L : nullptr;
+        for (int e = ct; e < L * L; e += 128) {
+          const float a = ((bt ? __ldg(bt + e) : 0.f) + (mt ? __ldg(mt + e) : 0.f)) * 1.4426950408889634f;
+          const int r = u * 64 + e / L, j = e % L;
+          uint8_t* dst = sAdd + (r >> 3) * 1024 + (r & 7) * 128 + ((((j >> 3) ^ (r & 7))) << 4) + (j & 7) * 2;
+          *reinterpret_cast<__half*>(dst) = __float2half_rn(a);
         }
-        __half2 h2 = __floats2half2_rn(a, b);
-        addh[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
       }
+      named_sync(3, 128);
     }
     float inv_prev = 0.f;
     for (int i = 0; i <= n_local; ++i) {
@@ -255,14 +264,21 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         if constexpr (ADD) {
           // t = scale*log2e*S + (bias+mask)*log2e, kept in s[]
 #pragma unroll
-          for (int j = 0; j < 64; j += 2) {
-            const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&addh[j >> 1]));
-            const float t0 = fmaf(__uint_as_float(s[j]), scale_log2, a.x);
-            const float t1 = fmaf(__uint_as_float(s[j + 1]), scale_log2, a.y);
-            s[j] = __float_as_uint(t0);
-            s[j + 1] = __float_as_uint(t1);
-            if (j < L) mx = fmaxf(mx, t0);
-            if (j + 1 < L) mx = fmaxf(mx, t1);
+          for (int c = 0; c < 8; ++c) {
+            if (LK > 0 && 8 * c >= LK) break;
+            const uint4 av = *reinterpret_cast<const uint4*>(arow + ((c ^ aswz) << 4));
+            const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int j = 8 * c + 2 * t;
+              const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&aw[t]));
+              const float t0 = fmaf(__uint_as_float(s[j]), scale_log2, a.x);
+              const float t1 = fmaf(__uint_as_float(s[j + 1]), scale_log2, a.y);
+              s[j] = __float_as_uint(t0);
+              s[j + 1] = __float_as_uint(t1);
+              if (j < L) mx = fmaxf(mx, t0);
+              if (j + 1 < L) mx = fmaxf(mx, t1);
+            }
           }
         } else {
 #pragma unroll
@@ -366,7 +382,7 @@ int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void*
   if ((rc = get_units_map(&mv, v, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
   if ((rc = get_units_map(&mo, o, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
   auto kern = fwd_tc_kernel<T, D, LK, ADD>;
-  constexpr int smem = Cfg<D>::kSmem;
+  constexpr int smem = Cfg<D, ADD>::kSmem;
   static bool attr_done = false;
   if (!attr_done) {
     rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
@@ -375,7 +391,7 @@ int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void*
     attr_done = true;
   }
   const int n_tiles = (int)((g.units + 1) / 2);
-  const int per_sm = Cfg<D>::kCtasPerSm;
+  const int per_sm = Cfg<D, ADD>::kCtasPerSm;
   int grid = std::max(1, std::min(n_tiles, device_sm_count() * per_sm));
   if (ADD && n_tiles > grid) {
     const int pt = add_period_tiles(g, bias != nullptr, mask != nullptr);
