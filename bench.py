@@ -5,15 +5,20 @@ fp16 forward of all 12 window-attention layers (depths 2/2/6/2):
   stage 1 (8192, 3, 49, 32) x2, stage 2 (2048, 6, 49, 32) x2,
   stage 3 (512, 12, 49, 32) x6, stage 4 (128, 24, 49, 32) x2   [(N, h, L, d)]
 One "step" = those 12 forward calls, each on its own resident Q/K/V (1.46 GB
-of algorithmic traffic per step, > 10x the 126 MB L2, so no flush is needed).
-value = windows processed per second over all ranks (window = all h heads).
+of algorithmic traffic per step, > 10x the 126 MB L2, so no flush is needed),
+replayed from a CUDA graph. value = windows processed per second over all
+ranks (a window = all h heads of one window).
+
+The same line carries "fwd_bwd": BASELINE configs[2] (Swin-T B=128, bf16,
+relative-position bias on every layer (learnable: dBias computed), shifted-window
+mask on the SW-MSA layers, forward + backward) measured the same way.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fwa|reference]
-                  [--workload swin_t_fwd|swin_t_fwdbwd|swin_b_fwdbwd]
+                  [--workload swin_t_fwd|swin_t_fwdbwd|swin_b_fwdbwd|large_sweep]
 
-Multi-GPU: torchrun, one process per GPU, weak scaling (B=128 per rank), no
+Multi-GPU: torchrun, one process per GPU, weak scaling (B images per rank), no
 collective on the hot path; barrier + synchronize around the timed region,
-time = max over ranks.
+time = max over ranks (all_reduce MAX).
 """
 
 from __future__ import annotations
@@ -35,31 +40,41 @@ SWIN_T = [(8192, 3, 49, 32)] * 2 + [(2048, 6, 49, 32)] * 2 + [(512, 12, 49, 32)]
          [(128, 24, 49, 32)] * 2  # B=128, 224^2, window 7
 SWIN_B384 = [(4096, 4, 144, 32)] * 2 + [(1024, 8, 144, 32)] * 2 + [(256, 16, 144, 32)] * 18 + \
             [(64, 32, 144, 32)] * 2  # B=64, 384^2, window 12
+LARGE = [(61035, 1, 64, 32), (30517, 1, 64, 64), (15258, 1, 256, 32), (7629, 1, 256, 64)]
 WORKLOADS = {
-    # name: (layers, images per rank, windows per image per stage-1, dtype, passes, mask/bias)
-    "swin_t_fwd": dict(layers=SWIN_T, batch=128, dtype="float16", bwd=False, extras=False,
-                       k=7, hw=56, desc="Swin-T 224^2 B=128, 12 layers, fp16 forward (configs[1])"),
-    "swin_t_fwdbwd": dict(layers=SWIN_T, batch=128, dtype="bfloat16", bwd=True, extras=True,
-                          k=7, hw=56, desc="Swin-T 224^2 B=128, shifted-window mask + rel-pos "
-                                           "bias, bf16 forward+backward (configs[2])"),
+    "swin_t_fwd": dict(layers=SWIN_T, batch=128, dtype="float16", bwd=False, extras=False, k=7,
+                       desc="Swin-T 224^2 B=128, 12 layers, fp16 forward (configs[1])"),
+    "swin_t_fwdbwd": dict(layers=SWIN_T, batch=128, dtype="bfloat16", bwd=True, extras=True, k=7,
+                          desc="Swin-T 224^2 B=128, rel-pos bias (learnable) + shifted-window "
+                               "mask on SW-MSA layers, bf16 forward+backward (configs[2])"),
     "swin_b_fwdbwd": dict(layers=SWIN_B384, batch=64, dtype="float16", bwd=True, extras=False,
-                          k=12, hw=96, desc="Swin-B 384^2 window 12 B=64, fp16 forward+backward "
-                                            "(configs[3])"),
+                          k=12, desc="Swin-B 384^2 window 12 B=64, fp16 forward+backward "
+                                     "(configs[3])"),
+    "large_sweep": dict(layers=LARGE, batch=1, dtype="float16", bwd=False, extras=False, k=8,
+                        desc="large-window sweep L=64/256, d=32/64, ~1 GB per call, fp16 "
+                             "forward (configs[4])"),
 }
+METRIC = "window-attn windows/s + % HBM roofline"
 
 
 def load_peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(p) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def load_ncu_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 # ---------------------------------------------------------------------------
-# nvidia-smi clock sampler (runs during warm-up + timed region)
+# nvidia-smi clock sampler (runs during the clock soak + timed region)
 # ---------------------------------------------------------------------------
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -115,18 +130,14 @@ class ClockSampler:
 # CPU reference (oracle port of flash.py Alg. 1/2, float64) on host cores
 # ---------------------------------------------------------------------------
 def _cpu_worker(args):
-    layers, batch, n_images, extras, bwd, seed = args
-    import numpy as np
-
+    layers, batch, n_images, bwd, seed = args
     from oracle import flashwin_oracle as orc
 
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     rng = orc.Rng(seed)
     spent = 0.0
     windows = 0
     for (N, h, L, d) in layers:
-        per_img = N // batch
-        n = per_img * n_images
+        n = max(1, N // batch) * n_images
         q, kk, v = (orc.fill_uniform(rng, (n, h, L, d)) for _ in range(3))
         do = orc.fill_uniform(rng, (n, h, L, d)) if bwd else None
         r = max(1, d // 16)
@@ -140,44 +151,253 @@ def _cpu_worker(args):
 
 
 def cpu_reference(wl, seconds_target=12.0, steps=1, warmup=0):
-    """Time the oracle port on all host cores; returns windows/s (+ sample description)."""
+    """Time the oracle port on all host cores; returns (windows/s, cores, sample, s/step)."""
     import multiprocessing as mp
 
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     os.environ["OMP_NUM_THREADS"] = "1"
     cores = len(os.sched_getaffinity(0))
     layers = wl["layers"]
-    # calibrate: one image through all layers on one core
-    w, t = _cpu_worker((layers, wl["batch"], 1, wl["extras"], wl["bwd"], 1))
-    per_proc_images = max(1, int(seconds_target / max(t, 1e-3) / max(steps + warmup, 1)))
-    ctx = mp.get_context("fork")
+    _, t = _cpu_worker((layers, wl["batch"], 1, wl["bwd"], 1))
+    per_proc = max(1, int(seconds_target / max(t, 1e-3) / max(steps + warmup, 1)))
     results = []
-    with ctx.Pool(cores) as pool:
+    with mp.get_context("fork").Pool(cores) as pool:
         for s in range(warmup + steps):
-            outs = pool.map(_cpu_worker, [(layers, wl["batch"], per_proc_images, wl["extras"],
-                                           wl["bwd"], 100 + i) for i in range(cores)])
-            dt = max(o[1] for o in outs)  # slowest process's compute time
+            outs = pool.map(_cpu_worker, [(layers, wl["batch"], per_proc, wl["bwd"], 100 + i)
+                                          for i in range(cores)])
             if s >= warmup:
-                results.append((sum(o[0] for o in outs), dt))
+                results.append((sum(o[0] for o in outs), max(o[1] for o in outs)))
     windows = sum(r[0] for r in results)
     secs = sum(r[1] for r in results)
-    sample = (f"{per_proc_images} image(s) x {cores} processes per step through all "
-              f"{len(layers)} layers, float64 oracle port of flash.py Alg.1"
-              f"{'/2' if wl['bwd'] else ''} (numpy, 1 BLAS thread per process)")
+    sample = (f"{per_proc} image(s) x {cores} processes per step through all {len(layers)} "
+              f"layers, float64 oracle port of flash.py Alg.1{'/2' if wl['bwd'] else ''} "
+              f"(numpy, 1 BLAS thread per process; windows/s = windows / slowest process time)")
     return windows / secs, cores, sample, secs / max(len(results), 1)
 
 
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def run_gpu(args, wl):
+class GpuWorkload:
+    def __init__(self, wl, dev, seed):
+        import torch
+
+        import paper_2501_06480_b200 as fwa
+        from paper_2501_06480_b200 import ops
+
+        self.wl, self.dev, self.ops = wl, dev, ops
+        self.dtype = getattr(torch, wl["dtype"])
+        self.eb = torch.empty((), dtype=self.dtype).element_size()
+        layers, k = wl["layers"], wl["k"]
+        rng = fwa.Rng(seed)
+        self.bufs = []
+        for (N, h, L, d) in layers:
+            q, kk, v = (fwa.fill_uniform(rng, (N, h, L, d), dtype=self.dtype, device=dev)
+                        for _ in range(3))
+            do = fwa.fill_uniform(rng, (N, h, L, d), dtype=self.dtype, device=dev) \
+                if wl["bwd"] else None
+            bias = mask = None
+            if wl["extras"]:
+                table = fwa.fill_uniform(rng, ((2 * k - 1) ** 2, h), -0.04, 0.04, device=dev)
+                bias = ops.bias_gather(table, k)
+                # Swin alternates W-MSA / SW-MSA: the second block of each pair is shifted
+                # and masked; the last stage (a single 7x7 window) never shifts.
+                nW = N // wl["batch"]
+                side = int(round(math.sqrt(nW))) * k
+                idx_in_stage = sum(1 for x in layers[:len(self.bufs)] if x == (N, h, L, d))
+                if nW > 1 and idx_in_stage % 2 == 1:
+                    mask = ops.shift_mask(side, side, k, k // 2, device=dev)
+            o = torch.empty_like(q)
+            self.bufs.append((q, kk, v, do, bias, mask, o, d ** -0.5))
+        torch.cuda.synchronize()
+
+    def layer(self, i, fwd=True, bwd=None):
+        q, kk, v, do, bias, mask, o, sc = self.bufs[i]
+        if fwd:
+            self.ops.attention_forward(q, kk, v, sc, bias, mask, out=o)
+        if self.wl["bwd"] if bwd is None else bwd:
+            self.ops.attention_backward(q, kk, v, do, sc, bias, mask, want_dbias=bias is not None)
+
+    def step(self):
+        for i in range(len(self.bufs)):
+            self.layer(i)
+
+    def bytes_per_step(self):
+        fwd = sum(4 * N * h * L * d * self.eb for (N, h, L, d) in self.wl["layers"])
+        bwd = sum(7 * N * h * L * d * self.eb for (N, h, L, d) in self.wl["layers"]) \
+            if self.wl["bwd"] else 0
+        return fwd + bwd
+
+    def flops_per_step(self):
+        f = sum(4 * N * h * L * L * d for (N, h, L, d) in self.wl["layers"])
+        if self.wl["bwd"]:
+            f += sum(10 * N * h * L * L * d for (N, h, L, d) in self.wl["layers"])
+        return f
+
+
+def timed_graph(torch, nat, work, steps, warmup, eager, soak_s, world, dist):
+    for _ in range(warmup):
+        work.step()
+    torch.cuda.synchronize()
+    graph, per_step = None, None
+    if not eager:
+        graph = torch.cuda.CUDAGraph()
+        l0 = nat.launch_count()
+        with torch.cuda.graph(graph):
+            work.step()
+        per_step = nat.launch_count() - l0
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else work.step
+    t_soak = time.perf_counter()
+    while time.perf_counter() - t_soak < soak_s:
+        for _ in range(10):
+            run()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = nat.launch_count()
+    start.record()
+    for _ in range(steps):
+        run()
+    stop.record()
+    torch.cuda.synchronize()
+    launches = per_step * steps if graph is not None else nat.launch_count() - l0
+    ms = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([ms], device=work.dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    del graph
+    return ms / steps, launches
+
+
+def flushed_launch_ms(torch, work, i, fwd, bwd, reps=5):
+    """Median device time of one layer launch with L2 flushed before it.
+
+    The flush READS a 512 MB buffer (a sum), so L2 is refilled with clean lines:
+    no dirty flush data is written back while the timed kernel runs.
+    """
+    flush = torch.ones(512 * 1024 * 1024 // 4, dtype=torch.float32, device=work.dev)
+    times = []
+    for _ in range(reps + 1):
+        flush.sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        work.layer(i, fwd=fwd, bwd=bwd)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    del flush
+    return statistics.median(times[1:])
+
+
+def measure(args, name, dev, rank, world, dist, steps, with_e2e):
     import torch
-    import torch.distributed as dist
 
     import paper_2501_06480_b200 as fwa
     from paper_2501_06480_b200 import _native as nat
-    from paper_2501_06480_b200 import ops
 
+    wl = WORKLOADS[name]
+    work = GpuWorkload(wl, dev, 42 + rank)
+    ms_step, launches = timed_graph(torch, nat, work, steps, args.warmup, args.eager,
+                                    args.soak_s, world, dist)
+    peak, peak_src = load_peaks()
+    layers = wl["layers"]
+    windows = sum(N for (N, h, L, d) in layers)
+    byts = work.bytes_per_step()
+    # dominant layer (most bytes) timed alone with a cold L2: the roofline numerator
+    dom = max(range(len(layers)), key=lambda i: math.prod(layers[i]))
+    N, h, L, d = layers[dom]
+    unit_bytes = N * h * L * d * work.eb
+    fp = fwa.ops.footprint(N, h, L, d, work.dtype)
+    fwd_ms = flushed_launch_ms(torch, work, dom, True, False)
+    kern = {"fwd": {"shape": [N, h, L, d], "ms": fwd_ms, "GB/s": 4 * unit_bytes / fwd_ms / 1e6,
+                    "kernel": fp["kernel_fwd"]}}
+    if wl["bwd"]:
+        bwd_ms = flushed_launch_ms(torch, work, dom, False, True)
+        kern["bwd"] = {"shape": [N, h, L, d], "ms": bwd_ms, "GB/s": 7 * unit_bytes / bwd_ms / 1e6,
+                       "kernel": fp["kernel_bwd"],
+                       "note": "includes the deterministic dBias reduce" if wl["extras"] else ""}
+    mk = "bwd" if wl["bwd"] else "fwd"
+    ncu = load_ncu_traffic().get(f"{name}:{mk}") or {}
+    mult = 7 if mk == "bwd" else 4
+    roof = {"bound": "hbm", "achieved": kern[mk]["GB/s"], "peak": peak, "unit": "GB/s",
+            "frac": kern[mk]["GB/s"] / peak,
+            "traffic": ncu.get("dram_bytes_per_launch"),
+            "traffic_source": ncu.get("source", "no committed ncu capture for this launch"),
+            "peak_source": peak_src,
+            "kernel": f"{mk} ({kern[mk]['kernel']}) on the dominant layer {kern[mk]['shape']}",
+            "algorithmic_bytes_per_launch": mult * unit_bytes,
+            "bytes_per_unit": f"{mult}*L*d*{work.eb} = {mult * L * d * work.eb} B",
+            "how": "CUDA events around one eager launch on the launching stream, L2 flushed "
+                   "(512 MB read) before each launch, median of 5",
+            "launches": kern,
+            "step_frac": byts / (ms_step / 1e3) / 1e9 / peak}
+    out = {"value": windows * world / (ms_step / 1e3), "ms_per_step": ms_step,
+           "tflops": work.flops_per_step() * world / (ms_step / 1e3) / 1e12,
+           "hbm_frac_step": byts / (ms_step / 1e3) / 1e9 / peak, "roofline": roof,
+           "gpu_launches": launches, "algorithmic_bytes_per_step": byts}
+    if with_e2e:
+        out["e2e"] = e2e(args, work, world, dist)
+    del work
+    torch.cuda.empty_cache()
+    return out
+
+
+def e2e(args, work, world, dist):
+    """Same metric through the public API on pinned HOST buffers (H2D + kernels + D2H)."""
+    import torch
+
+    import paper_2501_06480_b200 as fwa
+
+    wl = work.wl
+    host = [tuple(t.cpu().pin_memory() if t is not None else None for t in (q, kk, v, do))
+            for (q, kk, v, do, _, _, _, _) in work.bufs]
+    r = max(1, wl["layers"][0][3] // 16)
+
+    def run():
+        for (qh, kh, vh, doh), (_, _, _, _, bias, mask, _, sc) in zip(host, work.bufs):
+            cfg = fwa.TileConfig(r=r, scale=sc)
+            _, ctx, _ = fwa.batched_flash_forward(qh, kh, vh, cfg, [fwa.ScratchpadArena(1 << 20)],
+                                                  bias=bias, mask=mask)
+            if wl["bwd"]:
+                fwa.batched_flash_backward(ctx, doh, [fwa.ScratchpadArena(1 << 20)])
+    run()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    for _ in range(n):
+        run()
+    torch.cuda.synchronize()
+    s = (time.perf_counter() - t0) / n
+    if world > 1:
+        t = torch.tensor([s], device=work.dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        s = float(t.item())
+    per = [N * h * L * d * work.eb for (N, h, L, d) in wl["layers"]]
+    return {"value": sum(N for (N, h, L, d) in wl["layers"]) * world / s, "unit": "windows/s",
+            "h2d_bytes_per_step": (4 if wl["bwd"] else 3) * sum(per),
+            "d2h_bytes_per_step": (3 if wl["bwd"] else 1) * sum(per),
+            "path": "paper_2501_06480_b200.batched_flash_forward"
+                    f"{'/batched_flash_backward' if wl['bwd'] else ''} on pinned host torch "
+                    "tensors: chunked H2D / kernel / D2H overlapped on three streams, results "
+                    "returned in host memory", "steps": n}
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_06480_b200 import _native as nat
+
+    wl = WORKLOADS[args.workload]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -186,234 +406,74 @@ def run_gpu(args, wl):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     nat.load()
-    dtype = getattr(torch, wl["dtype"])
-    eb = torch.empty((), dtype=dtype).element_size()
-    layers = wl["layers"]
-    k = wl["k"]
-    # per-rank inputs: every layer has its own resident Q/K/V(/dO)
-    rng = fwa.Rng(42 + rank)
-    bufs = []
-    for (N, h, L, d) in layers:
-        q, kk, v = (fwa.fill_uniform(rng, (N, h, L, d), dtype=dtype, device=dev) for _ in range(3))
-        do = fwa.fill_uniform(rng, (N, h, L, d), dtype=dtype, device=dev) if wl["bwd"] else None
-        bias = mask = None
-        if wl["extras"]:
-            table = fwa.fill_uniform(rng, ((2 * k - 1) ** 2, h), -0.04, 0.04, device=dev)
-            bias = ops.bias_gather(table, k)
-            # Swin alternates W-MSA / SW-MSA: the second block of each pair is shifted and
-            # masked; the last stage (7x7 map = one window) never shifts.
-            nW = N // wl["batch"]
-            side = int(round(math.sqrt(nW))) * k
-            idx_in_stage = sum(1 for x in layers[:len(bufs)] if x == (N, h, L, d))
-            if nW > 1 and idx_in_stage % 2 == 1:
-                mask = ops.shift_mask(side, side, k, k // 2, device=dev)
-        o = torch.empty_like(q)
-        bufs.append((q, kk, v, do, bias, mask, o, d ** -0.5))
-    torch.cuda.synchronize()
-
-    def step():
-        for i, (q, kk, v, do, bias, mask, o, sc) in enumerate(bufs):
-            ops.attention_forward(q, kk, v, sc, bias, mask, out=o)
-            if wl["bwd"]:
-                ops.attention_backward(q, kk, v, do, sc, bias, mask, want_dbias=bias is not None)
-
-    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
-                           if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit()
-                           else local)
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+    sampler = ClockSampler(int(vis[local]) if len(vis) > local and vis[local].isdigit() else local)
     sampler.start()
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    # One step = the 12 layer calls, captured once into a CUDA graph (launch-bound
-    # small stages would otherwise measure Python/ctypes time, not the GPU).
-    graph = None
-    per_step_launches = None
-    if not args.eager:
-        graph = torch.cuda.CUDAGraph()
-        l0 = nat.launch_count()
-        with torch.cuda.graph(graph):
-            step()
-        per_step_launches = nat.launch_count() - l0
-        for _ in range(3):
-            graph.replay()
-        torch.cuda.synchronize()
-    # clock soak: keep the GPU busy ~1.5 s so nvidia-smi samples the loaded clocks
-    t_soak = time.perf_counter()
-    while time.perf_counter() - t_soak < args.soak_s:
-        for _ in range(20):
-            graph.replay() if graph is not None else step()
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = nat.launch_count()
-    start.record()
-    for s in range(args.steps):
-        if graph is not None:
-            graph.replay()
-        else:
-            step()
-    stop.record()
-    torch.cuda.synchronize()
-    launches = nat.launch_count() - launches0
-    if graph is not None:
-        launches = per_step_launches * args.steps
-    elapsed_ms = start.elapsed_time(stop)
-    if world > 1:
-        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
-        dist.barrier()
+    main_res = measure(args, args.workload, dev, rank, world, dist, args.steps, not args.no_e2e)
+    extra = None
+    if args.workload == "swin_t_fwd" and not args.no_extra:
+        extra = measure(args, "swin_t_fwdbwd", dev, rank, world, dist, max(3, args.steps // 2),
+                        False)
     clocks = sampler.stop()
-
-    # Per-layer kernel durations (roofline numerator): each distinct layer shape
-    # replayed R times inside its own graph, CUDA events around the replays.
-    reps = 10
-    per_shape = {}
-    for i, lay in enumerate(layers):
-        if lay in per_shape:
-            continue
-        q, kk, v, do, bias, mask, o, sc = bufs[i]
-        g1 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g1):
-            for _ in range(reps):
-                ops.attention_forward(q, kk, v, sc, bias, mask, out=o)
-                if wl["bwd"]:
-                    ops.attention_backward(q, kk, v, do, sc, bias, mask, want_dbias=bias is not None)
-        g1.replay()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        g1.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        per_shape[lay] = e0.elapsed_time(e1) / reps
-        del g1
-    per_layer_ms = [per_shape[lay] for lay in layers]
-    windows_per_step = sum(N for (N, h, L, d) in layers)
-    fwd_bytes = [4 * N * h * L * d * eb for (N, h, L, d) in layers]
-    bwd_bytes = [7 * N * h * L * d * eb for (N, h, L, d) in layers] if wl["bwd"] else [0] * len(layers)
-    alg_bytes_step = sum(fwd_bytes) + sum(bwd_bytes)
-    flops_step = sum(4 * N * h * L * L * d for (N, h, L, d) in layers) + \
-        (sum(10 * N * h * L * L * d for (N, h, L, d) in layers) if wl["bwd"] else 0)
-    ms_per_step = elapsed_ms / args.steps
-    value = windows_per_step * world / (ms_per_step / 1e3)
-    peak, peak_src = load_peaks()
-    kernel_ms = sum(per_layer_ms)
-    achieved = alg_bytes_step / (kernel_ms / 1e3) / 1e9
-    # dominant launch: the stage-1 layers (largest units count)
-    dom = max(range(len(layers)), key=lambda i: fwd_bytes[i] + bwd_bytes[i])
-    dom_gbs = (fwd_bytes[dom] + bwd_bytes[dom]) / (per_layer_ms[dom] / 1e3) / 1e9
-    fp = ops.footprint(*layers[0], dtype=dtype)
-
-    # ---- e2e through the public API with pinned host buffers --------------
-    e2e = None
-    if not args.no_e2e:
-        host = []
-        for (q, kk, v, do, bias, mask, o, sc) in bufs:
-            host.append(tuple(t.cpu().pin_memory() if t is not None else None for t in (q, kk, v, do)))
-        cfg_r = max(1, layers[0][3] // 16)
-
-        def e2e_step():
-            res = []
-            for (qh, kh, vh, doh), (_, _, _, _, bias, mask, _, sc) in zip(host, bufs):
-                cfg = fwa.TileConfig(r=cfg_r, scale=sc)
-                o, ctx, _ = fwa.batched_flash_forward(qh, kh, vh, cfg, [fwa.ScratchpadArena(1 << 20)],
-                                                      bias=bias, mask=mask)
-                res.append(o)
-                if wl["bwd"]:
-                    res.extend(fwa.batched_flash_backward(ctx, doh, [fwa.ScratchpadArena(1 << 20)])[:3])
-            return res
-        e2e_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e2e_steps = max(1, min(args.steps, args.e2e_steps))
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            e2e_step()
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        n_in = 4 if wl["bwd"] else 3
-        n_out = 4 if wl["bwd"] else 1
-        per_layer = [N * h * L * d * eb for (N, h, L, d) in layers]
-        e2e = {"value": windows_per_step * world / e2e_s, "unit": "windows/s",
-               "h2d_bytes_per_step": n_in * sum(per_layer), "d2h_bytes_per_step": n_out * sum(per_layer),
-               "path": "paper_2501_06480_b200.batched_flash_forward"
-                       f"{'/batched_flash_backward' if wl['bwd'] else ''} on pinned host torch "
-                       "tensors (H2D copy + kernels + D2H of the outputs)",
-               "steps": e2e_steps}
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v_cpu, cores, sample, _ = cpu_reference(wl, seconds_target=args.cpu_seconds)
-        cpu = {"value": v_cpu, "unit": "windows/s", "cores": cores, "kind": "port", "sample": sample}
-
+        v, cores, sample, _ = cpu_reference(wl, seconds_target=args.cpu_seconds)
+        cpu = {"value": v, "unit": "windows/s", "cores": cores, "kind": "port", "sample": sample}
     if rank == 0:
         line = {
-            "metric": "window-attn windows/s (Swin-T B=128 fp16 fwd, 12 layers)"
-            if args.workload == "swin_t_fwd" else f"window-attn windows/s ({wl['desc']})",
-            "value": value, "unit": "windows/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": {"float16": "f16", "bfloat16": "bf16"}[wl["dtype"]],
-            "data": "synthetic (SplitMix64 U[-1,1), seed 42+rank)",
-            "config": {"workload": args.workload, "desc": wl["desc"], "images_per_gpu": wl["batch"],
-                       "layers": [list(x) for x in layers], "global_batch": wl["batch"] * world,
-                       "parallelism": f"dp{world} (weak: {wl['batch']} images per GPU, no collective)",
-                       "launch": "eager" if args.eager else "CUDA graph of one step (12 layer calls), PDL between kernels",
-                       "l2": "no flush: each step streams "
-                             f"{alg_bytes_step / 1e9:.2f} GB of distinct tensors (>> 126 MB L2)"},
-            "tflops": flops_step * world / (ms_per_step / 1e3) / 1e12,
-            "hbm_frac_step": alg_bytes_step / (ms_per_step / 1e3) / 1e9 / peak,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                         "kernel": f"fwa_{'fwd+bwd' if wl['bwd'] else 'fwd'} ({fp['kernel_fwd']})",
-                         "algorithmic_bytes_per_step": alg_bytes_step,
-                         "dominant_launch": {"shape": list(layers[dom]), "ms": per_layer_ms[dom],
-                                             "GB/s": dom_gbs, "frac": dom_gbs / peak},
-                         "per_layer_ms": per_layer_ms,
-                         "how": "per-launch time = CUDA events around a graph of 10 back-to-back "
-                                "launches of that layer; achieved = algorithmic bytes / sum of "
-                                "per-layer launch times"},
-            "gpu_launches": launches,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "clocks": clocks,
+            "metric": f"{METRIC} ({wl['desc']})", "value": main_res["value"], "unit": "windows/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": main_res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": {"float16": "f16", "bfloat16": "bf16"}[wl["dtype"]],
+            "data": "synthetic (SplitMix64 U[-1,1), seed 42+rank; random bias table)",
+            "config": {"workload": args.workload, "desc": wl["desc"],
+                       "images_per_gpu": wl["batch"], "global_batch": wl["batch"] * world,
+                       "layers": [list(x) for x in wl["layers"]],
+                       "parallelism": f"dp{world} (weak: {wl['batch']} images per GPU, "
+                                      "no collective on the hot path)",
+                       "launch": "eager" if args.eager else
+                                 "one step captured in a CUDA graph, PDL between kernels",
+                       "l2": f"no flush for the step: "
+                             f"{main_res['algorithmic_bytes_per_step'] / 1e9:.2f} GB of distinct "
+                             "tensors per step (>> 126 MB L2); dominant-launch timing flushes L2 "
+                             "(512 MB read) before each launch"},
+            "tflops": main_res["tflops"], "hbm_frac_step": main_res["hbm_frac_step"],
+            "roofline": main_res["roofline"], "gpu_launches": main_res["gpu_launches"],
+            "e2e": main_res.get("e2e"), "cpu_baseline": cpu, "clocks": clocks,
         }
+        if extra is not None:
+            line["fwd_bwd"] = {"workload": "swin_t_fwdbwd",
+                               "desc": WORKLOADS["swin_t_fwdbwd"]["desc"],
+                               "value": extra["value"], "unit": "windows/s",
+                               "ms_per_step": extra["ms_per_step"], "dtype": "bf16",
+                               "hbm_frac_step": extra["hbm_frac_step"], "tflops": extra["tflops"],
+                               "roofline": extra["roofline"], "gpu_launches": extra["gpu_launches"]}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_reference(args, wl):
+def run_reference(args):
+    wl = WORKLOADS[args.workload]
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     v, cores, sample, per_step = cpu_reference(wl, seconds_target=args.cpu_seconds,
                                                steps=args.steps, warmup=args.warmup)
-    line = {
-        "impl": "reference",
-        "metric": "window-attn windows/s (Swin-T B=128 fp16 fwd, 12 layers)"
-        if args.workload == "swin_t_fwd" else f"window-attn windows/s ({wl['desc']})",
-        "value": v, "unit": "windows/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (SplitMix64 U[-1,1))",
+    print(json.dumps({
+        "impl": "reference", "metric": f"{METRIC} ({wl['desc']})", "value": v,
+        "unit": "windows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64 U[-1,1))",
         "config": {"workload": args.workload, "desc": wl["desc"],
                    "note": "reference CPU path = oracle port (oracle/flashwin_oracle.py) of "
-                           "flash.py Alg.1/2 in float64 on all host cores; the reference itself is "
-                           "pure Python and is not shipped to the GPU box"},
+                           "flash.py Alg.1/2 in float64 on all host cores; the reference package "
+                           "is pure Python and is not shipped to the GPU box"},
         "cpu_baseline": {"value": v, "unit": "windows/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "windows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line))
+    }))
 
 
 def main():
@@ -427,16 +487,15 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the embedded fwd+bwd line")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the timed steps")
-    ap.add_argument("--soak-s", type=float, default=1.5, help="loaded seconds before timing (clock sampling)")
+    ap.add_argument("--soak-s", type=float, default=1.5, help="loaded seconds before timing")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3  # timing rule: at least 3 warm-up steps
-    wl = WORKLOADS[args.workload]
+    args.warmup = max(args.warmup, 3)  # timing rule: at least 3 warm-up steps
     if args.impl == "reference":
-        run_reference(args, wl)
+        run_reference(args)
     else:
-        run_gpu(args, wl)
+        run_gpu(args)
 
 
 if __name__ == "__main__":
