@@ -129,14 +129,17 @@ int pick_fwd(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask, int
 
 int pick_bwd(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask, bool want_dbias,
              int* kernel, size_t* smem, int* tmem) {
-  const bool tc_ok = tc_bwd_supported(g, d->dtype, has_bias, has_mask, want_dbias);
+  const bool tc_small = tc_bwd_supported(g, d->dtype, has_bias, has_mask, want_dbias);
+  const bool tc_large =
+      !tc_small && tc_bwd_large_supported(g, d->dtype, has_bias, has_mask, want_dbias);
+  const bool tc_ok = tc_small || tc_large;
   if (d->kernel == FWA_KERNEL_TC && !tc_ok)
     return fail(FWA_ERR_CAPACITY, "tcgen05 backward does not support this shape/dtype (L=" +
                                       std::to_string(g.L) + ", d=" + std::to_string(g.d) + ")");
   if (tc_ok && d->kernel != FWA_KERNEL_GENERIC) {
     *kernel = FWA_KERNEL_TC;
-    *smem = tc_bwd_smem(g);
-    *tmem = tc_bwd_tmem_cols(g);
+    *smem = tc_small ? tc_bwd_smem(g) : tc_bwd_large_smem(g);
+    *tmem = tc_small ? tc_bwd_tmem_cols(g) : 512;
     return FWA_OK;
   }
   *kernel = FWA_KERNEL_GENERIC;
@@ -255,9 +258,12 @@ extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const
   if (need && (!workspace || workspace_bytes < need))
     return fail(FWA_ERR_CAPACITY, "backward workspace needs " + std::to_string(need) +
                                       " bytes, got " + std::to_string(workspace_bytes));
-  if (kern == FWA_KERNEL_TC)
-    return launch_bwd_tc(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
-                         (float*)workspace, (cudaStream_t)stream);
+  if (kern == FWA_KERNEL_TC) {
+    if (tc_bwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr, dbias != nullptr))
+      return launch_bwd_tc(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
+                           (float*)workspace, (cudaStream_t)stream);
+    return launch_bwd_tc_large(g, desc->dtype, q, k, v, dout, dq, dk, dv, (cudaStream_t)stream);
+  }
   return launch_bwd_generic(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
                             (float*)workspace, (cudaStream_t)stream);
 }

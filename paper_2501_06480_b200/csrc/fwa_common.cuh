@@ -113,6 +113,12 @@ int launch_bwd_tc(const Geom& g, int dtype, const void* q, const void* k, const 
                   const void* dout, const float* bias, const float* mask, void* dq, void* dk,
                   void* dv, float* dbias, float* ws, cudaStream_t s);
 
+// tcgen05 / TMA backward for 64 < L <= 256 (fwa_tc_bwd_large.cu)
+bool tc_bwd_large_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias);
+size_t tc_bwd_large_smem(const Geom& g);
+int launch_bwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                        const void* dout, void* dq, void* dk, void* dv, cudaStream_t s);
+
 int device_sm_count();
 int64_t device_l2_bytes();
 size_t device_max_smem_optin();

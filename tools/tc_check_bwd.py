@@ -8,7 +8,8 @@ from paper_2501_06480_b200 import ops, _native
 torch.manual_seed(0)
 for dt in (torch.float16, torch.bfloat16):
     for (N, h, L, d) in [(1, 2, 64, 32), (1, 1, 49, 32), (4, 3, 49, 32), (5, 3, 49, 32), (2, 2, 64, 64),
-                         (3, 1, 16, 16), (700, 3, 49, 32), (8192, 3, 49, 32), (33, 5, 36, 64)]:
+                         (3, 1, 16, 16), (700, 3, 49, 32), (8192, 3, 49, 32), (33, 5, 36, 64),
+                         (64, 4, 144, 32), (100, 2, 256, 32), (37, 3, 128, 64), (50, 2, 100, 16), (33, 1, 81, 32), (61, 2, 200, 16), (4096, 4, 144, 32)]:
         q, k, v, do = (torch.rand(N, h, L, d, device="cuda").mul_(2).sub_(1).to(dt) for _ in range(4))
         sc = d ** -0.5
         qf, kf, vf = (t.float().requires_grad_() for t in (q, k, v))
