@@ -80,6 +80,9 @@ int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k,
 int get_units_map(CUtensorMap* out, const void* ptr, int dtype, int64_t units, int L, int d,
                   int box_rows, int box_units);
 
+// FWA_NO_PDL=1 in the environment disables PDL (diagnostics).
+bool pdl_enabled();
+
 // Launch with programmatic dependent launch (PDL) enabled: the kernel must execute
 // griddepcontrol.wait before touching global memory.
 template <typename... KArgs, typename... Args>
@@ -94,7 +97,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

@@ -1,6 +1,7 @@
 // fwa_host.cu — host helpers shared by the TMA kernels: tensor-map encode + cache, PDL launch.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -94,6 +95,14 @@ int get_units_map(CUtensorMap* out, const void* ptr, int dtype, int64_t units, i
   if (map_cache().size() > 1024) map_cache().clear();
   map_cache().emplace(key, *out);
   return FWA_OK;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("FWA_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
 }
 
 }  // namespace fwa

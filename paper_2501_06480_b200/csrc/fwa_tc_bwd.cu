@@ -430,7 +430,7 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
                           __uint_as_float(acc[t + 2]), __uint_as_float(acc[t + 3]));
       }
     }
-    if (leader) bulk_wait<0>();
+    if (leader) bulk_wait_read<0>();  // smem reads done; the grid's completion flushes the writes
   }
   tc_fence_before();
   __syncthreads();

@@ -355,7 +355,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
       }
       inv_prev = inv_cur;
     }
-    if (leader) bulk_wait<0>();
+    if (leader) bulk_wait_read<0>();  // smem reads done; the grid's completion flushes the writes
   }
   tc_fence_before();
   __syncthreads();
