@@ -54,20 +54,23 @@ template <int D, bool ADD = false>
 struct Cfg {
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTileBytes = kTileRows * kRowBytes;            // one of Q/K/V per stage
-  // with bias/mask, 16 KB of smem hold the CTA's (bias + mask) rows: one stage fewer
-  static constexpr int kStages = D <= 16 ? (ADD ? 6 : 8) : (ADD ? 3 : 4);
-  static constexpr int kAddBytes = ADD ? 128 * 128 : 0;
+  static constexpr int kStages = D <= 16 ? 8 : 4;
+  // staging for the O tile; with bias/mask it also stages one unit's f16 add table
+  // (64 x 64) once in the prologue, so it is at least 8 KB
+  static constexpr int kStageO = (ADD && kTileRows * D * 2 < 8192) ? 8192 : kTileRows * D * 2;
   static constexpr int kCtasPerSm = D <= 32 ? 2 : 1;
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);  // UMMA layout code
-  static constexpr int kSmem = 1024 /*align slack*/ + kStages * 3 * kTileBytes +
-                               kTileBytes /*O staging*/ + kAddBytes + 256 /*barriers*/;
+  static constexpr int kSmem = 1024 /*align slack*/ + kStages * 3 * kTileBytes + kStageO +
+                               256 /*barriers*/;
   static constexpr int kChunks = kRowBytes / 16;  // 16-byte chunks per row
   // TMEM columns (lane = tile row; unit 0 rows are lanes 0-63, unit 1 rows 64-127):
   //   S [0,64) fp32 | P [64,96) 16-bit pairs | O0, O1 (d each) fp32.
   // Each unit's S/P/O occupy the SAME columns in its own 64 lanes: the MMAs for
   // unit 0 and unit 1 run with complementary disable-output-lane masks.
   static constexpr uint32_t kTmemP = 64, kTmemO0 = 96, kTmemO1 = 96 + D;
-  static constexpr uint32_t kTmemCols = 256;
+  // (bias + mask) * log2e rows of the CTA's two unit slots, fp32, loaded once (ADD)
+  static constexpr uint32_t kTmemAdd = 96 + 2 * D;
+  static constexpr uint32_t kTmemCols = (kTmemAdd + (ADD ? 64 : 0) <= 256) ? 256 : 512;
 };
 
 struct SmemBarriers {
@@ -104,8 +107,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
   uint8_t* sK = sQ + C::kStages * C::kTileBytes;
   uint8_t* sV = sK + C::kStages * C::kTileBytes;
   uint8_t* sO = sV + C::kStages * C::kTileBytes;   // 1 staging tile for the TMA store
-  uint8_t* sAdd = sO + C::kTileBytes;              // [128 rows][64] f16 add rows (ADD)
-  SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(sAdd + C::kAddBytes);
+  SmemBarriers* bars = reinterpret_cast<SmemBarriers*>(sO + C::kStageO);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -221,16 +223,14 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
     uint8_t* orow = sO + row * C::kRowBytes;
     const uint32_t oswz = (uint32_t)((row * C::kRowBytes) >> 7) & (C::kChunks - 1);
     const bool leader = (threadIdx.x == 64);
-    const uint32_t aswz = (uint32_t)(row & 7);
-    uint8_t* arow = sAdd + (row >> 3) * 1024 + (row & 7) * 128;
     if constexpr (ADD) {
-      // Cooperative, coalesced fill of the CTA's two (bias + mask) * log2e tiles
-      // (every tile of this CTA has the same (w, h) pair per slot): f16, swizzled rows.
+      // Load the CTA's two (bias + mask) * log2e tiles into TMEM once: every tile of this
+      // CTA has the same (w, h) pair per slot (period-aligned grid). Each unit's table is
+      // read coalesced into the (not yet used) staging tile as f16, then each thread
+      // moves its own row to its TMEM lane as fp32.
       const int ct = threadIdx.x - 64;             // 0..127 within the softmax warps
-      for (int i = ct; i < 2 * 64 * 64 / 2; i += 128)
-        reinterpret_cast<uint32_t*>(sAdd)[i] = 0u;
-      named_sync(3, 128);
-#pragma unroll
+      const uint32_t rswz = (uint32_t)(row & 7);
+#pragma unroll 1
       for (int u = 0; u < 2; ++u) {
         const int uu = 2 * (int)blockIdx.x + u;
         const int hd = uu % add.heads;
@@ -238,13 +238,33 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         const float* __restrict__ bt = add.bias ? add.bias + (size_t)hd * L * L : nullptr;
         const float* __restrict__ mt = add.mask ? add.mask + (size_t)w * L * L : nullptr;
         for (int e = ct; e < L * L; e += 128) {
-          const float a = ((bt ? __ldg(bt + e) : 0.f) + (mt ? __ldg(mt + e) : 0.f)) * 1.4426950408889634f;
-          const int r = u * 64 + e / L, j = e % L;
-          uint8_t* dst = sAdd + (r >> 3) * 1024 + (r & 7) * 128 + ((((j >> 3) ^ (r & 7))) << 4) + (j & 7) * 2;
-          *reinterpret_cast<__half*>(dst) = __float2half_rn(a);
+          const float av = ((bt ? __ldg(bt + e) : 0.f) + (mt ? __ldg(mt + e) : 0.f)) * 1.4426950408889634f;
+          const int r = e / L, j = e % L;
+          *reinterpret_cast<__half*>(sO + r * 128 + ((((j >> 3) ^ (r & 7))) << 4) + (j & 7) * 2) =
+              __float2half_rn(av);
         }
+        named_sync(3, 128);
+        if (ul == u) {
+          const int r = row & 63;
+          uint32_t fv[64];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 hv = *reinterpret_cast<const uint4*>(sO + r * 128 + ((c ^ rswz) << 4));
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int j = 8 * c + 2 * t;
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hw[t]));
+              fv[j] = __float_as_uint((r < L && j < L) ? f.x : 0.f);
+              fv[j + 1] = __float_as_uint((r < L && j + 1 < L) ? f.y : 0.f);
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g) tmem_st16(tmem + t_lane + C::kTmemAdd + g * 16, &fv[g * 16]);
+          tmem_wait_st();
+        }
+        named_sync(3, 128);
       }
-      named_sync(3, 128);
     }
     float inv_prev = 0.f;
     for (int i = 0; i <= n_local; ++i) {
@@ -253,10 +273,15 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         mbar_wait(&bars->s_full, i & 1);
         tc_fence_after();
         uint32_t s[64];
+        uint32_t ad[ADD ? 64 : 1];
 #pragma unroll
         for (int g = 0; g < 4; ++g)
-          if (LK == 0 || g * 16 < LK)
+          if (LK == 0 || g * 16 < LK) {
             tmem_ld16(tmem + t_lane + g * 16, *reinterpret_cast<uint32_t(*)[16]>(&s[g * 16]));
+            if constexpr (ADD)
+              tmem_ld16(tmem + t_lane + C::kTmemAdd + g * 16,
+                        *reinterpret_cast<uint32_t(*)[16]>(&ad[g * 16]));
+          }
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&bars->s_empty);
@@ -264,21 +289,10 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         if constexpr (ADD) {
           // t = scale*log2e*S + (bias+mask)*log2e, kept in s[]
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            if (LK > 0 && 8 * c >= LK) break;
-            const uint4 av = *reinterpret_cast<const uint4*>(arow + ((c ^ aswz) << 4));
-            const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const int j = 8 * c + 2 * t;
-              const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&aw[t]));
-              const float t0 = fmaf(__uint_as_float(s[j]), scale_log2, a.x);
-              const float t1 = fmaf(__uint_as_float(s[j + 1]), scale_log2, a.y);
-              s[j] = __float_as_uint(t0);
-              s[j + 1] = __float_as_uint(t1);
-              if (j < L) mx = fmaxf(mx, t0);
-              if (j + 1 < L) mx = fmaxf(mx, t1);
-            }
+          for (int j = 0; j < 64; ++j) {
+            const float t0 = fmaf(__uint_as_float(s[j]), scale_log2, __uint_as_float(ad[j]));
+            s[j] = __float_as_uint(t0);
+            if (j < L) mx = fmaxf(mx, t0);
           }
         } else {
 #pragma unroll
