@@ -120,6 +120,21 @@ size_t fwa_bwd_workspace_bytes(const fwa_desc* desc, int want_dbias);
  * flash.py:84-103). Returns FWA_ERR_CAPACITY when no kernel can run the shape. */
 int fwa_footprint(const fwa_desc* desc, fwa_footprint_t* out);
 
+/* ---- fused layouts (no reference counterpart) ------- */
+
+/* Same math as fwa_fwd, reading Q/K/V straight from the Swin qkv-Linear output
+ * qkv [num_windows][seq_len][3][heads][head_dim] and writing O as
+ * [num_windows][seq_len][heads][head_dim] (the proj-Linear input): the two
+ * permute copies around window attention disappear. tcgen05 path only
+ * (seq_len <= 64, head_dim in {16,32,64}, f16/bf16); FWA_ERR_CAPACITY otherwise. */
+int fwa_fwd_qkv(const fwa_desc* desc, const void* qkv, const float* bias,
+                const float* mask, void* o, void* stream);
+
+/* Backward in the same layouts: dout [N][L][h][d] -> dqkv [N][L][3][h][d]. */
+int fwa_bwd_qkv(const fwa_desc* desc, const void* qkv, const void* dout,
+                const float* bias, const float* mask, void* dqkv, float* dbias,
+                void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- window partition / reverse (windowing.py:44-70) ------------------ */
 
 /* in [B][H][W][C] -> out [B*nW][k*k][C]; with shift s the image is first

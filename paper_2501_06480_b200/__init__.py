@@ -22,7 +22,16 @@ from .api import (
     flash_backward,
     flash_forward,
 )
-from .autograd import RelativePositionBias, WindowAttentionFunction, relative_position_bias, window_attention
+from .autograd import (
+    RelativePositionBias,
+    WindowAttentionFunction,
+    WindowAttentionQKVFunction,
+    partition_windows,
+    relative_position_bias,
+    reverse_windows,
+    window_attention,
+    window_attention_qkv,
+)
 from .errors import (
     CapacityError,
     ContextError,
@@ -69,6 +78,7 @@ __all__ = [
     "TileConfig",
     "TrafficReport",
     "WindowAttentionFunction",
+    "WindowAttentionQKVFunction",
     "WindowConfig",
     "batched_flash_backward",
     "batched_flash_forward",
@@ -78,10 +88,13 @@ __all__ = [
     "merge_reports",
     "ops",
     "peak_sram_backward",
+    "partition_windows",
     "peak_sram_forward",
     "relative_position_bias",
     "resolve_r",
+    "reverse_windows",
     "window_attention",
+    "window_attention_qkv",
     "window_partition",
     "window_reverse",
 ]

@@ -95,6 +95,11 @@ _SIGNATURES = {
         [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
          ctypes.c_size_t, _vp],
     ),
+    "fwa_fwd_qkv": (ctypes.c_int, [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, _vp, _vp]),
+    "fwa_bwd_qkv": (
+        ctypes.c_int,
+        [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp],
+    ),
     "fwa_bwd_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(FwaDesc), ctypes.c_int]),
     "fwa_footprint": (ctypes.c_int, [ctypes.POINTER(FwaDesc), ctypes.POINTER(FwaFootprint)]),
     "fwa_window_partition": (ctypes.c_int, [ctypes.POINTER(FwaWinDesc), _vp, _vp, _vp]),

@@ -267,3 +267,37 @@ extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const
   return launch_bwd_generic(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
                             (float*)workspace, (cudaStream_t)stream);
 }
+
+// ---- token-major ("qkv") layout: fused with the Swin qkv / proj Linears ----------
+// qkv: [N][L][3][h][d] (qkv-Linear output), o / dout: [N][L][h][d] (proj-Linear input),
+// dqkv: [N][L][3][h][d]. tcgen05 kernels only (L <= 64, d in {16,32,64}, f16/bf16):
+// other shapes return FWA_ERR_CAPACITY so the caller can fall back to fwa_fwd/fwa_bwd.
+extern "C" int fwa_fwd_qkv(const fwa_desc* desc, const void* qkv, const float* bias,
+                           const float* mask, void* o, void* stream) {
+  Geom g;
+  int rc = validate(desc, &g, true, mask);
+  if (rc) return rc;
+  if (!qkv || !o) return fail(FWA_ERR_SHAPE, "null qkv/o pointer");
+  if (!tc_fwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr))
+    return fail(FWA_ERR_CAPACITY, "fused qkv layout needs the tcgen05 forward (L <= 64, "
+                                  "d in {16,32,64}, f16/bf16)");
+  return launch_fwd_tc(g, desc->dtype, qkv, nullptr, nullptr, bias, mask, o,
+                       (cudaStream_t)stream, kTokens);
+}
+
+extern "C" int fwa_bwd_qkv(const fwa_desc* desc, const void* qkv, const void* dout,
+                           const float* bias, const float* mask, void* dqkv, float* dbias,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  Geom g;
+  int rc = validate(desc, &g, true, mask);
+  if (rc) return rc;
+  if (!qkv || !dout || !dqkv) return fail(FWA_ERR_SHAPE, "null qkv/dO/dqkv pointer");
+  if (!tc_bwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr, dbias != nullptr))
+    return fail(FWA_ERR_CAPACITY, "fused qkv layout needs the tcgen05 backward (L <= 64, "
+                                  "d in {16,32,64}, f16/bf16)");
+  const size_t need = fwa_bwd_workspace_bytes(desc, dbias != nullptr);
+  if (need && (!workspace || workspace_bytes < need))
+    return fail(FWA_ERR_CAPACITY, "backward workspace needs " + std::to_string(need) + " bytes");
+  return launch_bwd_tc(g, desc->dtype, qkv, nullptr, nullptr, dout, bias, mask, dqkv, nullptr,
+                       nullptr, dbias, (float*)workspace, (cudaStream_t)stream, kTokens);
+}

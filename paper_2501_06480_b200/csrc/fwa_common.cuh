@@ -74,11 +74,24 @@ size_t tc_fwd_smem(const Geom& g, int dtype);
 int tc_fwd_tmem_cols(const Geom& g);
 int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k,
                   const void* v, const float* bias, const float* mask, void* o,
-                  cudaStream_t s);
+                  cudaStream_t s, int layout = 0);
 
 // fwa_host.cu: cached 3-D tensor map over [units][L][d] 16-bit data
 int get_units_map(CUtensorMap* out, const void* ptr, int dtype, int64_t units, int L, int d,
                   int box_rows, int box_units);
+
+// 4-D map over a token-major [N][L][S][h][d] tensor (fused qkv / proj layouts).
+int get_tokens_map(CUtensorMap* out, const void* base, int dtype, int64_t N, int L, int S, int h,
+                   int d, int box_rows);
+
+// Operand layout of the TMA kernels: kUnits = [N][h][L][d] (the reference's batched
+// layout); kTokens = token-major, read from the packed qkv-Linear output [N][L][3][h][d]
+// and written as [N][L][h][d] (= the proj-Linear input): no permute copies.
+enum Layout { kUnits = 0, kTokens = 1 };
+struct LayoutArgs {
+  int mode;   // Layout
+  int heads;  // h (kTokens: unit u = (u / h, u % h))
+};
 
 // FWA_NO_PDL=1 in the environment disables PDL (diagnostics).
 bool pdl_enabled();
@@ -114,7 +127,7 @@ int tc_bwd_tmem_cols(const Geom& g);
 size_t tc_bwd_workspace_bytes(const Geom& g, bool has_mask, bool want_dbias);
 int launch_bwd_tc(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                   const void* dout, const float* bias, const float* mask, void* dq, void* dk,
-                  void* dv, float* dbias, float* ws, cudaStream_t s);
+                  void* dv, float* dbias, float* ws, cudaStream_t s, int layout = 0);
 
 // tcgen05 / TMA backward for 64 < L <= 256 (fwa_tc_bwd_large.cu)
 bool tc_bwd_large_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias);

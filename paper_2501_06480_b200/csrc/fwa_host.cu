@@ -97,6 +97,31 @@ int get_units_map(CUtensorMap* out, const void* ptr, int dtype, int64_t units, i
   return FWA_OK;
 }
 
+// 4-D map over a token-major tensor [N][L][S][h][d] (S = 3 for packed qkv, 1 for O/dO)
+// starting at `base` (already offset to the q/k/v slice): dims (d, h, L, N), box (d, 1, rows, 1).
+int get_tokens_map(CUtensorMap* out, const void* base, int dtype, int64_t N, int L, int S, int h,
+                   int d, int box_rows) {
+  EncodeFn enc = get_encode();
+  if (!enc) return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t gdim[4] = {(cuuint64_t)d, (cuuint64_t)h, (cuuint64_t)L, (cuuint64_t)N};
+  const cuuint64_t gstride[3] = {(cuuint64_t)d * 2, (cuuint64_t)S * h * d * 2,
+                                 (cuuint64_t)L * S * h * d * 2};
+  const cuuint32_t box[4] = {(cuuint32_t)d, 1, (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUtensorMapSwizzle swz = d == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : d == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = enc(out, dtype == FWA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   4, const_cast<void*>(base), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled (token layout) failed (" +
+                                  std::to_string((int)r) + ")");
+  return FWA_OK;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("FWA_NO_PDL");

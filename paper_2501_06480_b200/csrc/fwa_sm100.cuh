@@ -64,6 +64,53 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* s
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
+                                            int c1, int c2, int c3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* src, int c0, int c1,
+                                             int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// One tile = two (window, head) units of 64 rows. kUnits: one 3-D box over [units][L][d];
+// kTokens: one 4-D box per unit over [N][L][h][d]-strided data (heads may straddle windows).
+template <int UnitBytes>
+__device__ __forceinline__ void load_tile(void* dst, const CUtensorMap* m, uint64_t* bar, int tile,
+                                          int mode, int heads, uint64_t policy) {
+  if (mode == 0) {
+    tma_load_3d(dst, m, bar, 0, 0, 2 * tile, policy);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int unit = 2 * tile + u;
+      tma_load_4d(static_cast<uint8_t*>(dst) + u * UnitBytes, m, bar, 0, unit % heads, 0,
+                  unit / heads, policy);
+    }
+  }
+}
+template <int UnitBytes>
+__device__ __forceinline__ void store_tile(const CUtensorMap* m, const void* src, int tile, int mode,
+                                           int heads) {
+  if (mode == 0) {
+    tma_store_3d(m, src, 0, 0, 2 * tile);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int unit = 2 * tile + u;
+      tma_store_4d(m, static_cast<const uint8_t*>(src) + u * UnitBytes, 0, unit % heads, 0,
+                   unit / heads);
+    }
+  }
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {

@@ -94,7 +94,7 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
               const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dk,
               const __grid_constant__ CUtensorMap tm_dv, int n_tiles, int L_rt, float scale,
-              BwdAddArgs add, unsigned int* err_flags) {
+              BwdAddArgs add, LayoutArgs lay, unsigned int* err_flags) {
   using C = BCfg<D>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   const int L = LK > 0 ? LK : L_rt;
@@ -159,10 +159,11 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         const int st = i % C::kStages;
         mbar_wait(&bars->empty[st], ((i / C::kStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->full[st], C::kStageBytes);
-        tma_load_3d(slot(st, 0), &tm_q, &bars->full[st], 0, 0, 2 * tile, pol);
-        tma_load_3d(slot(st, 1), &tm_k, &bars->full[st], 0, 0, 2 * tile, pol);
-        tma_load_3d(slot(st, 2), &tm_v, &bars->full[st], 0, 0, 2 * tile, pol);
-        tma_load_3d(slot(st, 3), &tm_do, &bars->full[st], 0, 0, 2 * tile, pol);
+        constexpr int kUB = kUnitRows * C::kRowBytes;
+        load_tile<kUB>(slot(st, 0), &tm_q, &bars->full[st], tile, lay.mode, lay.heads, pol);
+        load_tile<kUB>(slot(st, 1), &tm_k, &bars->full[st], tile, lay.mode, lay.heads, pol);
+        load_tile<kUB>(slot(st, 2), &tm_v, &bars->full[st], tile, lay.mode, lay.heads, pol);
+        load_tile<kUB>(slot(st, 3), &tm_do, &bars->full[st], tile, lay.mode, lay.heads, pol);
       }
     }
   } else if (warp == 1) {
@@ -407,9 +408,10 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
       fence_proxy_async_smem();
       named_sync(1, 128);
       if (leader) {
-        tma_store_3d(&tm_dq, slot(st, 0), 0, 0, 2 * tile);
-        tma_store_3d(&tm_dk, slot(st, 1), 0, 0, 2 * tile);
-        tma_store_3d(&tm_dv, slot(st, 2), 0, 0, 2 * tile);
+        constexpr int kUB = kUnitRows * C::kRowBytes;
+        store_tile<kUB>(&tm_dq, slot(st, 0), tile, lay.mode, lay.heads);
+        store_tile<kUB>(&tm_dk, slot(st, 1), tile, lay.mode, lay.heads);
+        store_tile<kUB>(&tm_dv, slot(st, 2), tile, lay.mode, lay.heads);
         bulk_commit();
         bulk_wait_read<0>();
         mbar_arrive(&bars->empty[st]);   // stage may be refilled
@@ -483,12 +485,24 @@ int bwd_grid(const Geom& g, bool period_bias, bool has_mask) {
 template <typename T, int D, int LK, bool ADD, bool DBIAS>
 int launch_bwd_t(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                  const void* dout, const float* bias, const float* mask, void* dq, void* dk,
-                 void* dv, float* dbias, float* ws, cudaStream_t s) {
+                 void* dv, float* dbias, float* ws, int layout, cudaStream_t s) {
   CUtensorMap m[7];
-  const void* ptrs[7] = {q, k, v, dout, dq, dk, dv};
   int rc;
-  for (int i = 0; i < 7; ++i)
-    if ((rc = get_units_map(&m[i], ptrs[i], dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+  if (layout == kUnits) {
+    const void* ptrs[7] = {q, k, v, dout, dq, dk, dv};
+    for (int i = 0; i < 7; ++i)
+      if ((rc = get_units_map(&m[i], ptrs[i], dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+  } else {  // q = qkv [N][L][3][h][d], dout = [N][L][h][d], dq = dqkv [N][L][3][h][d]
+    const int64_t N = g.units / g.heads;
+    const size_t hdb = (size_t)g.heads * g.d * 2;
+    const uint8_t* qkv = static_cast<const uint8_t*>(q);
+    uint8_t* dqkv = static_cast<uint8_t*>(dq);
+    const void* src[7] = {qkv, qkv + hdb, qkv + 2 * hdb, dout, dqkv, dqkv + hdb, dqkv + 2 * hdb};
+    for (int i = 0; i < 7; ++i)
+      if ((rc = get_tokens_map(&m[i], src[i], dtype, N, g.L, i == 3 ? 1 : 3, g.heads, g.d,
+                               kUnitRows)))
+        return rc;
+  }
   auto kern = bwd_tc_kernel<T, D, LK, ADD, DBIAS>;
   constexpr int smem = BCfg<D>::kSmem;
   static bool attr_done = false;
@@ -501,8 +515,9 @@ int launch_bwd_t(const Geom& g, int dtype, const void* q, const void* k, const v
   const int n_tiles = (int)((g.units + 1) / 2);
   const int grid = bwd_grid<D>(g, ADD || DBIAS, mask != nullptr);
   BwdAddArgs add{bias, mask, ws, g.heads, mask ? g.mask_windows : 1};
+  LayoutArgs lay{layout, g.heads};
   rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, m[0], m[1], m[2], m[3],
-                             m[4], m[5], m[6], n_tiles, (int)g.L, g.scale, add,
+                             m[4], m[5], m[6], n_tiles, (int)g.L, g.scale, add, lay,
                              device_flags_ptr()),
                   "bwd_tc_kernel launch");
   if (rc) return rc;
@@ -520,33 +535,33 @@ int launch_bwd_t(const Geom& g, int dtype, const void* q, const void* k, const v
 template <typename T, int D, int LK>
 int bwd_dispatch_flags(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                        const void* dout, const float* b, const float* m, void* dq, void* dk,
-                       void* dv, float* db, float* ws, cudaStream_t s) {
+                       void* dv, float* db, float* ws, int lay, cudaStream_t s) {
   const bool add = b || m;
   if (db) {
-    return add ? launch_bwd_t<T, D, LK, true, true>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s)
-               : launch_bwd_t<T, D, LK, false, true>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
+    return add ? launch_bwd_t<T, D, LK, true, true>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s)
+               : launch_bwd_t<T, D, LK, false, true>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s);
   }
-  return add ? launch_bwd_t<T, D, LK, true, false>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s)
-             : launch_bwd_t<T, D, LK, false, false>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
+  return add ? launch_bwd_t<T, D, LK, true, false>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s)
+             : launch_bwd_t<T, D, LK, false, false>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s);
 }
 
 template <typename T, int D>
 int bwd_dispatch_l(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                    const void* dout, const float* b, const float* m, void* dq, void* dk, void* dv,
-                   float* db, float* ws, cudaStream_t s) {
-  if (g.L == 49) return bwd_dispatch_flags<T, D, 49>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
-  if (g.L == 64) return bwd_dispatch_flags<T, D, 64>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
-  return bwd_dispatch_flags<T, D, 0>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
+                   float* db, float* ws, int lay, cudaStream_t s) {
+  if (g.L == 49) return bwd_dispatch_flags<T, D, 49>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s);
+  if (g.L == 64) return bwd_dispatch_flags<T, D, 64>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s);
+  return bwd_dispatch_flags<T, D, 0>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s);
 }
 
 template <typename T>
 int bwd_dispatch_d(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                    const void* dout, const float* b, const float* m, void* dq, void* dk, void* dv,
-                   float* db, float* ws, cudaStream_t s) {
+                   float* db, float* ws, int lay, cudaStream_t s) {
   switch (g.d) {
-    case 16: return bwd_dispatch_l<T, 16>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
-    case 32: return bwd_dispatch_l<T, 32>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
-    case 64: return bwd_dispatch_l<T, 64>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, s);
+    case 16: return bwd_dispatch_l<T, 16>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s);
+    case 32: return bwd_dispatch_l<T, 32>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s);
+    case 64: return bwd_dispatch_l<T, 64>(g, dtype, q, k, v, dout, b, m, dq, dk, dv, db, ws, lay, s);
   }
   return fail(FWA_ERR_CAPACITY, "tcgen05 backward: unsupported head_dim");
 }
@@ -587,10 +602,10 @@ size_t tc_bwd_workspace_bytes(const Geom& g, bool has_mask, bool want_dbias) {
 
 int launch_bwd_tc(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                   const void* dout, const float* bias, const float* mask, void* dq, void* dk,
-                  void* dv, float* dbias, float* ws, cudaStream_t s) {
+                  void* dv, float* dbias, float* ws, cudaStream_t s, int layout) {
   return dtype == FWA_BF16
-             ? bwd_dispatch_d<__nv_bfloat16>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s)
-             : bwd_dispatch_d<__half>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
+             ? bwd_dispatch_d<__nv_bfloat16>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, layout, s)
+             : bwd_dispatch_d<__half>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, layout, s);
 }
 
 }  // namespace fwa

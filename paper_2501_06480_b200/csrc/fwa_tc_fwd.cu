@@ -96,7 +96,7 @@ template <typename T, int D, int LK, bool ADD>
 __global__ void __launch_bounds__(kThreads, Cfg<D, ADD>::kCtasPerSm)
 fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-              int n_tiles, int L_rt, float scale_log2, AddArgs add) {
+              int n_tiles, int L_rt, float scale_log2, AddArgs add, LayoutArgs lay) {
   using C = Cfg<D, ADD>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   const int L = LK > 0 ? LK : L_rt;
@@ -153,9 +153,10 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         const uint32_t round = i / C::kStages;
         mbar_wait(&bars->empty[st], (round & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->full[st], 3 * C::kTileBytes);
-        tma_load_3d(sQ + st * C::kTileBytes, &tm_q, &bars->full[st], 0, 0, 2 * tile, pol);
-        tma_load_3d(sK + st * C::kTileBytes, &tm_k, &bars->full[st], 0, 0, 2 * tile, pol);
-        tma_load_3d(sV + st * C::kTileBytes, &tm_v, &bars->full[st], 0, 0, 2 * tile, pol);
+        constexpr int kUB = kUnitRows * C::kRowBytes;
+        load_tile<kUB>(sQ + st * C::kTileBytes, &tm_q, &bars->full[st], tile, lay.mode, lay.heads, pol);
+        load_tile<kUB>(sK + st * C::kTileBytes, &tm_k, &bars->full[st], tile, lay.mode, lay.heads, pol);
+        load_tile<kUB>(sV + st * C::kTileBytes, &tm_v, &bars->full[st], tile, lay.mode, lay.heads, pol);
       }
     }
   } else if (warp == 1) {
@@ -363,7 +364,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         fence_proxy_async_smem();
         named_sync(2, 128);
         if (leader) {
-          tma_store_3d(&tm_o, sO, 0, 0, 2 * tile);
+          store_tile<kUnitRows * C::kRowBytes>(&tm_o, sO, tile, lay.mode, lay.heads);
           bulk_commit();
         }
       }
@@ -388,13 +389,23 @@ int add_period_tiles(const Geom& g, bool has_bias, bool has_mask) {
 
 template <typename T, int D, int LK, bool ADD>
 int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
-             const float* bias, const float* mask, cudaStream_t s) {
+             const float* bias, const float* mask, int layout, cudaStream_t s) {
   CUtensorMap mq, mk, mv, mo;
   int rc;
-  if ((rc = get_units_map(&mq, q, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
-  if ((rc = get_units_map(&mk, k, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
-  if ((rc = get_units_map(&mv, v, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
-  if ((rc = get_units_map(&mo, o, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+  if (layout == kUnits) {
+    if ((rc = get_units_map(&mq, q, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+    if ((rc = get_units_map(&mk, k, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+    if ((rc = get_units_map(&mv, v, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+    if ((rc = get_units_map(&mo, o, dtype, g.units, g.L, g.d, kUnitRows, 2))) return rc;
+  } else {  // q = packed qkv [N][L][3][h][d]; o = [N][L][h][d]
+    const int64_t N = g.units / g.heads;
+    const size_t hd = (size_t)g.heads * g.d;
+    const uint8_t* qkv = static_cast<const uint8_t*>(q);
+    if ((rc = get_tokens_map(&mq, qkv, dtype, N, g.L, 3, g.heads, g.d, kUnitRows))) return rc;
+    if ((rc = get_tokens_map(&mk, qkv + hd * 2, dtype, N, g.L, 3, g.heads, g.d, kUnitRows))) return rc;
+    if ((rc = get_tokens_map(&mv, qkv + hd * 4, dtype, N, g.L, 3, g.heads, g.d, kUnitRows))) return rc;
+    if ((rc = get_tokens_map(&mo, o, dtype, N, g.L, 1, g.heads, g.d, kUnitRows))) return rc;
+  }
   auto kern = fwd_tc_kernel<T, D, LK, ADD>;
   constexpr int smem = Cfg<D, ADD>::kSmem;
   static bool attr_done = false;
@@ -413,8 +424,9 @@ int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void*
   }
   const float scale_log2 = g.scale * 1.4426950408889634f;
   AddArgs add{bias, mask, g.heads, mask ? g.mask_windows : 1};
+  LayoutArgs lay{layout, g.heads};
   rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, s, mq, mk, mv, mo, n_tiles,
-                             (int)g.L, scale_log2, add),
+                             (int)g.L, scale_log2, add, lay),
                   "fwd_tc_kernel launch");
   if (rc) return rc;
   count_launch();
@@ -423,23 +435,23 @@ int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void*
 
 template <typename T, int D, bool ADD>
 int dispatch_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
-               const float* b, const float* m, cudaStream_t s) {
-  if (g.L == 49) return launch_t<T, D, 49, ADD>(g, dtype, q, k, v, o, b, m, s);
-  if (g.L == 64) return launch_t<T, D, 64, ADD>(g, dtype, q, k, v, o, b, m, s);
-  return launch_t<T, D, 0, ADD>(g, dtype, q, k, v, o, b, m, s);
+               const float* b, const float* m, int lay, cudaStream_t s) {
+  if (g.L == 49) return launch_t<T, D, 49, ADD>(g, dtype, q, k, v, o, b, m, lay, s);
+  if (g.L == 64) return launch_t<T, D, 64, ADD>(g, dtype, q, k, v, o, b, m, lay, s);
+  return launch_t<T, D, 0, ADD>(g, dtype, q, k, v, o, b, m, lay, s);
 }
 
 template <typename T>
 int dispatch_d(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
-               const float* b, const float* m, cudaStream_t s) {
+               const float* b, const float* m, int lay, cudaStream_t s) {
   const bool add = b || m;
   switch (g.d) {
-    case 16: return add ? dispatch_l<T, 16, true>(g, dtype, q, k, v, o, b, m, s)
-                        : dispatch_l<T, 16, false>(g, dtype, q, k, v, o, b, m, s);
-    case 32: return add ? dispatch_l<T, 32, true>(g, dtype, q, k, v, o, b, m, s)
-                        : dispatch_l<T, 32, false>(g, dtype, q, k, v, o, b, m, s);
-    case 64: return add ? dispatch_l<T, 64, true>(g, dtype, q, k, v, o, b, m, s)
-                        : dispatch_l<T, 64, false>(g, dtype, q, k, v, o, b, m, s);
+    case 16: return add ? dispatch_l<T, 16, true>(g, dtype, q, k, v, o, b, m, lay, s)
+                        : dispatch_l<T, 16, false>(g, dtype, q, k, v, o, b, m, lay, s);
+    case 32: return add ? dispatch_l<T, 32, true>(g, dtype, q, k, v, o, b, m, lay, s)
+                        : dispatch_l<T, 32, false>(g, dtype, q, k, v, o, b, m, lay, s);
+    case 64: return add ? dispatch_l<T, 64, true>(g, dtype, q, k, v, o, b, m, lay, s)
+                        : dispatch_l<T, 64, false>(g, dtype, q, k, v, o, b, m, lay, s);
   }
   return fail(FWA_ERR_CAPACITY, "tcgen05 forward: unsupported head_dim");
 }
@@ -468,10 +480,10 @@ int tc_fwd_tmem_cols(const Geom& g) {
 }
 
 int launch_fwd_tc(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                  const float* bias, const float* mask, void* o, cudaStream_t s) {
+                  const float* bias, const float* mask, void* o, cudaStream_t s, int layout) {
   const bool bf = dtype == FWA_BF16;
-  return bf ? dispatch_d<__nv_bfloat16>(g, dtype, q, k, v, o, bias, mask, s)
-            : dispatch_d<__half>(g, dtype, q, k, v, o, bias, mask, s);
+  return bf ? dispatch_d<__nv_bfloat16>(g, dtype, q, k, v, o, bias, mask, layout, s)
+            : dispatch_d<__half>(g, dtype, q, k, v, o, bias, mask, layout, s);
   return fail(FWA_ERR_CAPACITY, "tcgen05 forward: unsupported head_dim");
 }
 

@@ -226,3 +226,81 @@ def fill_uniform_(out: torch.Tensor, state: int, lo: float = -1.0, hi: float = 1
                                          _stream(out.device))
     nat.check(st)
     return out
+
+
+# ---- fused Swin layouts (qkv-Linear output in, proj-Linear input out) -------------
+def _qkv_view(qkv: torch.Tensor, heads: int):
+    if qkv.dim() == 3:
+        N, L, C3 = qkv.shape
+        if C3 % (3 * heads):
+            raise ShapeError(f"qkv last dim {C3} is not 3*heads*d for heads={heads}")
+        qkv = qkv.view(N, L, 3, heads, C3 // (3 * heads))
+    if qkv.dim() != 5 or qkv.shape[2] != 3 or qkv.shape[3] != heads:
+        raise ShapeError(f"qkv must be (N, L, 3, heads, d) or (N, L, 3*heads*d), got {tuple(qkv.shape)}")
+    if not (qkv.is_cuda and qkv.is_contiguous()):
+        raise ShapeError("qkv must be a contiguous CUDA tensor")
+    return qkv
+
+
+def _split_qkv(qkv5):
+    """Device-side permute (fallback for shapes without the fused kernel)."""
+    q, k, v = (qkv5[:, :, i].permute(0, 2, 1, 3).contiguous() for i in range(3))
+    return q, k, v
+
+
+def attention_forward_qkv(qkv: torch.Tensor, heads: int, scale: float = 1.0, bias=None, mask=None,
+                          kernel: str = "auto") -> torch.Tensor:
+    """O (N, L, heads*d) from the packed qkv (N, L, 3*heads*d): Swin's qkv -> attn -> proj glue.
+
+    The tcgen05 kernel reads Q/K/V in place and writes O in the proj layout (no permutes);
+    shapes it does not take go through device permutes + attention_forward.
+    """
+    qkv5 = _qkv_view(qkv, heads)
+    N, L, _, h, d = qkv5.shape
+    mw = _check_bias_mask((N, h, L, d), qkv.device, bias, mask)
+    o = torch.empty((N, L, h * d), dtype=qkv.dtype, device=qkv.device)
+    if kernel != "generic" and qkv.dtype in (torch.float16, torch.bfloat16):
+        desc = make_desc(N, h, L, d, qkv.dtype, scale, 1, mw, kernel)
+        with torch.cuda.device(qkv.device):
+            st = nat.load().fwa_fwd_qkv(ctypes.byref(desc), _ptr(qkv5), _ptr(bias), _ptr(mask),
+                                        _ptr(o), _stream(qkv.device))
+        if st == 0:
+            return o
+        if st != 2 or kernel == "tc":
+            nat.check(st)
+    q, k, v = _split_qkv(qkv5)
+    out = attention_forward(q, k, v, scale, bias, mask, kernel="generic" if kernel == "generic" else "auto")
+    o.copy_(out.permute(0, 2, 1, 3).reshape(N, L, h * d))
+    return o
+
+
+def attention_backward_qkv(qkv: torch.Tensor, do: torch.Tensor, heads: int, scale: float = 1.0,
+                           bias=None, mask=None, kernel: str = "auto", want_dbias: bool = False):
+    """(dqkv (N, L, 3*heads*d), dBias-or-None) for dO in the proj layout (N, L, heads*d)."""
+    qkv5 = _qkv_view(qkv, heads)
+    N, L, _, h, d = qkv5.shape
+    if tuple(do.shape) != (N, L, h * d) or not do.is_contiguous() or do.dtype != qkv.dtype:
+        raise ShapeError(f"dO must be contiguous {qkv.dtype} (N, L, heads*d) = {(N, L, h * d)}")
+    mw = _check_bias_mask((N, h, L, d), qkv.device, bias, mask)
+    dqkv = torch.empty((N, L, 3 * h * d), dtype=qkv.dtype, device=qkv.device)
+    dbias = torch.empty((h, L, L), dtype=torch.float32, device=qkv.device) if want_dbias else None
+    if kernel != "generic" and qkv.dtype in (torch.float16, torch.bfloat16):
+        desc = make_desc(N, h, L, d, qkv.dtype, scale, 1, mw, kernel)
+        lib = nat.load()
+        ws_bytes = int(lib.fwa_bwd_workspace_bytes(ctypes.byref(desc), int(want_dbias)))
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=qkv.device) if ws_bytes else None
+        with torch.cuda.device(qkv.device):
+            st = lib.fwa_bwd_qkv(ctypes.byref(desc), _ptr(qkv5), _ptr(do), _ptr(bias), _ptr(mask),
+                                 _ptr(dqkv), _ptr(dbias), _ptr(ws), ctypes.c_size_t(ws_bytes),
+                                 _stream(qkv.device))
+        if st == 0:
+            return dqkv, dbias
+        if st != 2 or kernel == "tc":
+            nat.check(st)
+    q, k, v = _split_qkv(qkv5)
+    do4 = do.view(N, L, h, d).permute(0, 2, 1, 3).contiguous()
+    dq, dk, dv, db = attention_backward(q, k, v, do4, scale, bias, mask,
+                                        kernel="generic" if kernel == "generic" else "auto",
+                                        want_dbias=want_dbias)
+    dqkv.view(N, L, 3, h, d).copy_(torch.stack([t.permute(0, 2, 1, 3) for t in (dq, dk, dv)], dim=2))
+    return dqkv, db
