@@ -268,12 +268,18 @@ def timed_graph(torch, nat, work, steps, warmup, eager, soak_s, world, dist):
     launches = per_step * steps if graph is not None else nat.launch_count() - l0
     ms = start.elapsed_time(stop)
     if world > 1:
-        t = torch.tensor([ms], device=work.dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(torch, dist, ms, work.dev)
         dist.barrier()
     del graph
     return ms / steps, launches
+
+
+def max_over_ranks(torch, dist, x, dev):
+    """MAX all-reduce of a scalar (NCCL on the device; gloo on the host for the CPU smoke test)."""
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def flushed_launch_ms(torch, work, i, fwd, bwd, reps=5):
@@ -378,9 +384,7 @@ def e2e(args, work, world, dist):
     torch.cuda.synchronize()
     s = (time.perf_counter() - t0) / n
     if world > 1:
-        t = torch.tensor([s], device=work.dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        s = float(t.item())
+        s = max_over_ranks(torch, dist, s, work.dev)
     per = [N * h * L * d * work.eb for (N, h, L, d) in wl["layers"]]
     return {"value": sum(N for (N, h, L, d) in wl["layers"]) * world / s, "unit": "windows/s",
             "h2d_bytes_per_step": (4 if wl["bwd"] else 3) * sum(per),
@@ -401,10 +405,15 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; FWA_DIST_BACKEND=gloo lets several ranks share a GPU for a smoke test
+    backend = os.environ.get("FWA_DIST_BACKEND", "nccl")
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     nat.load()
     vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
     sampler = ClockSampler(int(vis[local]) if len(vis) > local and vis[local].isdigit() else local)
