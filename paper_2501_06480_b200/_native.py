@@ -21,7 +21,8 @@ from .errors import (
 )
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libfwa.so")
+# FWA_LIB_PATH: load an alternative build of the same C-ABI (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("FWA_LIB_PATH") or os.path.join(_HERE, "_lib", "libfwa.so")
 
 FWA_F32, FWA_F16, FWA_BF16 = 0, 1, 2
 KERNEL_AUTO, KERNEL_GENERIC, KERNEL_TC = 0, 1, 2

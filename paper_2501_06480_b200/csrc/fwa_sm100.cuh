@@ -152,6 +152,18 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
                : "memory");
 }
+// One lane of a converged warp (elect.sync). Issue tcgen05.mma / commit as
+// `if (elect_one()) mma(...);` from a warp whose 32 lanes all run the (uniform) control
+// flow: the compiler then keeps descriptors in uniform registers and emits the MMAs back
+// to back. From a `lane == 0` branch it has to wrap every MMA in an ELECT/R2UR.BROADCAST
+// waterfall loop, which costs ~100 cycles of issue per MMA.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }

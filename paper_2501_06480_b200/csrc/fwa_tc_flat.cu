@@ -1,0 +1,519 @@
+// fwa_tc_flat.cu — "flat-row" forward for large windows (64 < L <= 256, L % 16 == 0; e.g.
+// Swin-B 12x12 = 144, 16x16 = 256) on tcgen05 + TMA (sm_100a), f16/bf16, no bias/mask.
+//
+// For the [units][L][d] layout the units are contiguous, so Q/K/V/O are one flat
+// [units*L][d] row matrix. Each CTA owns a contiguous unit range [ua, ub) and walks
+// its rows in 128-row blocks that ignore unit boundaries: a block holds the tail of one
+// unit and the head of the next (<= 3 units for L < 128). Every TMEM lane therefore
+// carries a real query row — the per-unit tiling of fwa_tc_fwd_large.cu runs L=144 as a
+// 128-row tile plus a 16-row tile whose softmax leaves 3 of 4 warps idle.
+//
+//   S = Q_blk K_u^T   one lane-masked SS MMA chain per unit segment (lanes of the
+//                     segment written; tcgen05 disable-output-lane mask), N = L
+//   softmax           thread = row = TMEM lane; pass 1 row max, pass 2 ex2 + row sum,
+//                     P (16-bit pairs) written over the consumed S columns
+//   O = P V_u         lane-masked TS MMA chain per segment (A = P in TMEM), N = d,
+//                     into the S buffer's upper half (O_col = round_up(L/2, 16))
+//   epilogue          1/rowsum, convert, swizzled staging, TMA store (a CTA's last
+//                     block stores 16-row pieces so it never touches the next range)
+//
+// Two 256-column TMEM buffers and two softmax warpgroups ping-pong on alternate blocks:
+// the MMA warp issues S(b+1) before PV(b), so one group's softmax overlaps the other's
+// MMAs and epilogue. K/V of a unit are loaded once into a ring and released after the
+// PV of the last block that touches the unit. HBM: Q, K, V read once, O written once.
+#include <cuda.h>
+#include <math.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <numeric>
+
+#include "fwa_common.cuh"
+#include "fwa_sm100.cuh"
+
+#ifdef FWA_TRACE
+__device__ long long g_flat_trace[8][64];
+extern "C" int fwa_flat_trace_copy(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_flat_trace, sizeof(g_flat_trace));
+}
+#define FTRACE(ev, b)                                                      \
+  do {                                                                     \
+    if (blockIdx.x == 0 && (b) < 64) g_flat_trace[ev][b] = clock64();     \
+  } while (0)
+#else
+#define FTRACE(ev, b) \
+  do {                \
+  } while (0)
+#endif
+
+namespace fwa {
+namespace {
+
+using namespace sm100;
+
+constexpr int kFThreads = 320;  // producer, MMA, 2 x 4 softmax/epilogue warps
+constexpr int kRows = 128;
+
+// units intersecting one 128-row block: block starts are multiples of gcd(128, L) inside
+// a unit, so at most ceil((L - g + 128) / L) units.
+__host__ __device__ constexpr int max_segments(int L) {
+  return (L - std::gcd(128, L) + kRows + L - 1) / L;
+}
+
+template <int D, int L>
+struct FCfg {
+  static constexpr int kRowBytes = D * 2;
+  static constexpr int kQBytes = kRows * kRowBytes;
+  static constexpr int kKVBytes = L * kRowBytes;
+  static constexpr int kKVSlot = (kKVBytes + 1023) / 1024 * 1024;
+  static constexpr int kQStages = D >= 64 ? 2 : 4;
+  static constexpr int kFixed = 1024 + kQStages * kQBytes + 2 * kQBytes + 1024;
+  static constexpr int kKVAvail = (227 * 1024 - kFixed) / (2 * kKVSlot);
+  static constexpr int kKVStages = kKVAvail < 8 ? kKVAvail : 8;
+  static constexpr int kSmem = kFixed + kKVStages * 2 * kKVSlot;
+  static constexpr int kMaxSeg = max_segments(L);
+  static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
+  static constexpr int kChunks = kRowBytes / 16;
+  static constexpr uint32_t kOCol = ((L / 2 + 15) / 16) * 16;
+  static constexpr bool kFits = kKVStages >= 2 * kMaxSeg && kOCol + D <= 256 && kSmem <= 227 * 1024;
+};
+
+struct FBarriers {
+  uint64_t q_full[4], q_empty[4], kv_full[8], kv_empty[8];
+  uint64_t s_full[2], p_ready[2], o_full[2], buf_free[2];
+  uint32_t tmem_base;
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t fpack2(float a, float b) {
+  if constexpr (DT<T>::id == FWA_BF16) {
+    __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h2);
+  } else {
+    __half2 h2 = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h2);
+  }
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// tcgen05 disable-output-lane word w (lanes 32w..32w+31): bit set = lane outside [lo, hi)
+__device__ __forceinline__ uint32_t lane_off(int w, int lo, int hi) {
+  const int a = max(lo - 32 * w, 0), b = min(hi - 32 * w, 32);
+  if (b <= a) return 0xffffffffu;
+  const uint32_t in = (b - a == 32) ? 0xffffffffu : (((1u << (b - a)) - 1u) << a);
+  return ~in;
+}
+
+// 32 lanes x 32-bit, 32 consecutive columns
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+template <typename T, int D, int L>
+__global__ void __launch_bounds__(kFThreads, 1)
+fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                const __grid_constant__ CUtensorMap tm_o16, int64_t n_units, float scale_log2) {
+  using C = FCfg<D, L>;
+  constexpr bool kBF16 = DT<T>::id == FWA_BF16;
+  constexpr int QS = C::kQStages, KS = C::kKVStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sK = smem;                              // [KS] K slots
+  uint8_t* sV = sK + KS * C::kKVSlot;              // [KS] V slots
+  uint8_t* sQ = sV + KS * C::kKVSlot;              // [QS] Q blocks
+  uint8_t* sO = sQ + QS * C::kQBytes;              // [2] output staging (one per group)
+  FBarriers* bars = reinterpret_cast<FBarriers*>(sO + 2 * C::kQBytes);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // this CTA's unit range and its 128-row blocks
+  const int64_t ua = (int64_t)blockIdx.x * n_units / gridDim.x;
+  const int64_t ub = (int64_t)(blockIdx.x + 1) * n_units / gridDim.x;
+  const int r0 = (int)(ua * L), r1 = (int)(ub * L);
+  const int nblk = (r1 - r0 + kRows - 1) / kRows;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < QS; ++s) {
+      mbar_init(&bars->q_full[s], 1);
+      mbar_init(&bars->q_empty[s], 1);
+    }
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(&bars->kv_full[s], 1);
+      mbar_init(&bars->kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars->s_full[s], 1);
+      mbar_init(&bars->p_ready[s], 128);
+      mbar_init(&bars->o_full[s], 1);
+      mbar_init(&bars->buf_free[s], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_o);
+    tma_prefetch_desc(&tm_o16);
+  }
+  if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+  griddep_launch_dependents();
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0 && nblk > 0) {
+      griddep_wait();
+      const uint64_t pol = policy_evict_first();
+      int next = 0;  // next local unit to load
+      const int n_loc = (int)(ub - ua);
+      for (int b = 0; b < nblk; ++b) {
+        const int rs = r0 + b * kRows;
+        const int last = (min(rs + kRows, r1) - 1) / L - (int)ua;
+        for (; next <= last && next < n_loc; ++next) {
+          const int s = next % KS;
+          mbar_wait(&bars->kv_empty[s], ((next / KS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bars->kv_full[s], 2 * C::kKVBytes);
+          const int row = (int)((ua + next) * L);
+          tma_load_3d(sK + s * C::kKVSlot, &tm_k, &bars->kv_full[s], 0, row, 0, pol);
+          tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->kv_full[s], 0, row, 0, pol);
+        }
+        const int qs = b % QS;
+        mbar_wait(&bars->q_empty[qs], ((b / QS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->q_full[qs], C::kQBytes);
+        tma_load_3d(sQ + qs * C::kQBytes, &tm_q, &bars->q_full[qs], 0, rs, 0, pol);
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (whole warp runs the control flow, one elected lane issues) =====
+    if (nblk > 0) {
+      constexpr uint32_t idS = make_idesc_f16(kBF16, 128, L, false, false);
+      constexpr uint32_t idO = make_idesc_f16(kBF16, 128, D, false, true);
+      constexpr uint32_t sbo = 8 * C::kRowBytes;
+      auto issue_S = [&](int b) {
+        const int j = b & 1, qs = b % QS;
+        const int rs = r0 + b * kRows, re = min(rs + kRows, r1);
+        const int u0 = rs / L, u1 = (re - 1) / L;
+        mbar_wait(&bars->q_full[qs], (b / QS) & 1);
+        for (int u = u0; u <= u1; ++u) {
+          const int lu = u - (int)ua;
+          mbar_wait(&bars->kv_full[lu % KS], (lu / KS) & 1);
+        }
+        FTRACE(0, b);
+        if (b >= 2) mbar_wait(&bars->buf_free[j], ((b >> 1) - 1) & 1);
+        tc_fence_after();
+        FTRACE(1, b);
+        const uint32_t q0 = smem_u32(sQ + qs * C::kQBytes);
+        for (int u = u0; u <= u1; ++u) {
+          const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
+          const uint32_t m0 = lane_off(0, lo, hi), m1 = lane_off(1, lo, hi);
+          const uint32_t m2 = lane_off(2, lo, hi), m3 = lane_off(3, lo, hi);
+          const uint32_t k0 = smem_u32(sK + ((u - (int)ua) % KS) * C::kKVSlot);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            if (elect_one())
+              mma_f16_ss_m(tmem + j * 256, make_sdesc(q0 + kk * 32, 16, sbo, C::kSwz),
+                           make_sdesc(k0 + kk * 32, 16, sbo, C::kSwz), idS, kk > 0, m0, m1, m2, m3);
+          __syncwarp();
+        }
+        if (elect_one()) {
+          mma_commit(&bars->s_full[j]);
+          mma_commit(&bars->q_empty[qs]);
+        }
+        __syncwarp();
+      };
+      issue_S(0);
+      for (int b = 0; b < nblk; ++b) {
+        if (b + 1 < nblk) issue_S(b + 1);
+        const int j = b & 1;
+        const int rs = r0 + b * kRows, re = min(rs + kRows, r1);
+        const int u0 = rs / L, u1 = (re - 1) / L;
+        mbar_wait(&bars->p_ready[j], (b >> 1) & 1);
+        tc_fence_after();
+        FTRACE(2, b);
+        for (int u = u0; u <= u1; ++u) {
+          const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
+          const uint32_t m0 = lane_off(0, lo, hi), m1 = lane_off(1, lo, hi);
+          const uint32_t m2 = lane_off(2, lo, hi), m3 = lane_off(3, lo, hi);
+          const uint32_t v0 = smem_u32(sV + ((u - (int)ua) % KS) * C::kKVSlot);
+#pragma unroll
+          for (int kk = 0; kk < L / 16; ++kk)
+            if (elect_one())
+              mma_f16_ts_m(tmem + j * 256 + C::kOCol, tmem + j * 256 + kk * 8,
+                           make_sdesc(v0 + kk * 16 * C::kRowBytes, C::kKVSlot, sbo, C::kSwz), idO,
+                           kk > 0, m0, m1, m2, m3);
+          __syncwarp();
+        }
+        // units whose last block is b: their K/V slots may be refilled
+        const int nxt_u0 = (b + 1 < nblk) ? (rs + kRows) / L : u1 + 1;
+        if (elect_one()) {
+          mma_commit(&bars->o_full[j]);
+          for (int u = u0; u <= u1 && u < nxt_u0; ++u)
+            mma_commit(&bars->kv_empty[(u - (int)ua) % KS]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ===== softmax + epilogue: group g takes blocks b = g, g+2, ... =====
+    const int g = (warp - 2) >> 2;
+    const int qd = warp & 3;
+    const int r_in = qd * 32 + lane;
+    const uint32_t t_lane = (uint32_t)(qd * 32) << 16;
+    const uint32_t oswz = (uint32_t)((r_in * C::kRowBytes) >> 7) & (C::kChunks - 1);
+    uint8_t* stage = sO + g * C::kQBytes;
+    const bool leader = (warp & 3) == 0 && lane == 0;   // one thread per group
+    for (int b = g; b < nblk; b += 2) {
+      const int j = b & 1;
+      const uint32_t tb = tmem + t_lane + j * 256;
+      mbar_wait(&bars->s_full[j], (b >> 1) & 1);
+      tc_fence_after();
+      if (leader) FTRACE(3, b);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c0 = 0; c0 < L; c0 += 32) {           // pass 1: row max
+        uint32_t r[32];
+        if (c0 + 32 <= L) {
+          tmem_ld32(tb + c0, r);
+        } else {
+          tmem_ld16(tb + c0, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+        }
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 32; t += 2)
+          if (c0 + t < L) mx = fmax3(mx, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
+      }
+      const float mxs = mx * scale_log2;
+      float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < L; c0 += 32) {           // pass 2: p = 2^(s*c - m*c), P over S
+        uint32_t r[32];
+        if (c0 + 32 <= L) {
+          tmem_ld32(tb + c0, r);
+        } else {
+          tmem_ld16(tb + c0, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+        }
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          if (c0 + t < L) {
+            const float p0 = ex2(fmaf(__uint_as_float(r[t]), scale_log2, -mxs));
+            const float p1 = ex2(fmaf(__uint_as_float(r[t + 1]), scale_log2, -mxs));
+            sum0 += p0;
+            sum1 += p1;
+            pk[t >> 1] = fpack2<T>(p0, p1);
+          }
+        }
+        if (c0 + 32 <= L) {
+          tmem_st16(tb + c0 / 2, pk);
+        } else {
+          tmem_st8(tb + c0 / 2, pk);
+        }
+      }
+      tmem_wait_st();
+      if (leader) FTRACE(4, b);
+      const float inv = __frcp_rn(sum0 + sum1);
+      tc_fence_before();
+      mbar_arrive(&bars->p_ready[j]);
+
+      // ---- epilogue of block b ----
+      const int rs = r0 + b * kRows, nrows = min(kRows, r1 - rs);
+      mbar_wait(&bars->o_full[j], (b >> 1) & 1);
+      tc_fence_after();
+      if (leader) FTRACE(5, b);
+      uint32_t o[D];
+#pragma unroll
+      for (int q = 0; q < D / 16; ++q)
+        tmem_ld16(tb + C::kOCol + q * 16, *reinterpret_cast<uint32_t(*)[16]>(&o[q * 16]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars->buf_free[j]);
+      if (leader) bulk_wait_read<0>();           // previous store out of this staging buffer
+      named_sync(1 + g, 128);
+      uint8_t* orow = stage + r_in * C::kRowBytes;
+#pragma unroll
+      for (int c = 0; c < C::kChunks; ++c)
+        *reinterpret_cast<uint4*>(orow + ((c ^ oswz) << 4)) = make_uint4(
+            fpack2<T>(__uint_as_float(o[8 * c]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
+            fpack2<T>(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
+            fpack2<T>(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
+            fpack2<T>(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
+      fence_proxy_async_smem();
+      named_sync(3 + g, 128);
+      if (leader) {
+        if (nrows == kRows) {
+          tma_store_3d(&tm_o, stage, 0, rs, 0);
+        } else {
+          for (int t = 0; t < nrows; t += 16)
+            tma_store_3d(&tm_o16, stage + t * C::kRowBytes, 0, rs + t, 0);
+        }
+        bulk_commit();
+      }
+      if (leader) FTRACE(6, b);
+    }
+    if (leader) bulk_wait_read<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+template <typename T, int D, int L>
+int launch_flat_t(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
+                  cudaStream_t s) {
+  using C = FCfg<D, L>;
+  if constexpr (!C::kFits) {
+    return fail(FWA_ERR_CAPACITY, "flat forward: shape does not fit");
+  } else {
+    const int rows = (int)(g.units * L);
+    CUtensorMap m[5];
+    int rc;
+    if ((rc = get_units_map(&m[0], q, dtype, 1, rows, D, kRows, 1))) return rc;
+    if ((rc = get_units_map(&m[1], k, dtype, 1, rows, D, L, 1))) return rc;
+    if ((rc = get_units_map(&m[2], v, dtype, 1, rows, D, L, 1))) return rc;
+    if ((rc = get_units_map(&m[3], o, dtype, 1, rows, D, kRows, 1))) return rc;
+    if ((rc = get_units_map(&m[4], o, dtype, 1, rows, D, 16, 1))) return rc;
+    auto kern = fwd_flat_kernel<T, D, L>;
+    static bool attr_done = false;
+    if (!attr_done) {
+      rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem),
+                      "cudaFuncSetAttribute(fwd_flat)");
+      if (rc) return rc;
+      attr_done = true;
+    }
+    // every CTA gets >= 1 unit (ranges are balanced to within one unit)
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
+    rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kFThreads), (size_t)C::kSmem, s, m[0], m[1],
+                               m[2], m[3], m[4], (int64_t)g.units, g.scale * 1.4426950408889634f),
+                    "fwd_flat_kernel launch");
+    if (rc) return rc;
+    count_launch();
+    return FWA_OK;
+  }
+}
+
+template <typename T, int D>
+int flat_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
+           cudaStream_t s) {
+  switch (g.L) {
+    case 80: return launch_flat_t<T, D, 80>(g, dtype, q, k, v, o, s);
+    case 96: return launch_flat_t<T, D, 96>(g, dtype, q, k, v, o, s);
+    case 112: return launch_flat_t<T, D, 112>(g, dtype, q, k, v, o, s);
+    case 128: return launch_flat_t<T, D, 128>(g, dtype, q, k, v, o, s);
+    case 144: return launch_flat_t<T, D, 144>(g, dtype, q, k, v, o, s);
+    case 160: return launch_flat_t<T, D, 160>(g, dtype, q, k, v, o, s);
+    case 176: return launch_flat_t<T, D, 176>(g, dtype, q, k, v, o, s);
+    case 192: return launch_flat_t<T, D, 192>(g, dtype, q, k, v, o, s);
+    case 208: return launch_flat_t<T, D, 208>(g, dtype, q, k, v, o, s);
+    case 224: return launch_flat_t<T, D, 224>(g, dtype, q, k, v, o, s);
+    case 240: return launch_flat_t<T, D, 240>(g, dtype, q, k, v, o, s);
+    case 256: return launch_flat_t<T, D, 256>(g, dtype, q, k, v, o, s);
+  }
+  return fail(FWA_ERR_CAPACITY, "flat forward: unsupported L");
+}
+
+template <int D>
+constexpr bool fits_d(int L) {
+  switch (L) {
+    case 80: return FCfg<D, 80>::kFits;
+    case 96: return FCfg<D, 96>::kFits;
+    case 112: return FCfg<D, 112>::kFits;
+    case 128: return FCfg<D, 128>::kFits;
+    case 144: return FCfg<D, 144>::kFits;
+    case 160: return FCfg<D, 160>::kFits;
+    case 176: return FCfg<D, 176>::kFits;
+    case 192: return FCfg<D, 192>::kFits;
+    case 208: return FCfg<D, 208>::kFits;
+    case 224: return FCfg<D, 224>::kFits;
+    case 240: return FCfg<D, 240>::kFits;
+    case 256: return FCfg<D, 256>::kFits;
+  }
+  return false;
+}
+
+template <int D>
+constexpr int smem_d(int L) {
+  switch (L) {
+    case 80: return FCfg<D, 80>::kSmem;
+    case 96: return FCfg<D, 96>::kSmem;
+    case 112: return FCfg<D, 112>::kSmem;
+    case 128: return FCfg<D, 128>::kSmem;
+    case 144: return FCfg<D, 144>::kSmem;
+    case 160: return FCfg<D, 160>::kSmem;
+    case 176: return FCfg<D, 176>::kSmem;
+    case 192: return FCfg<D, 192>::kSmem;
+    case 208: return FCfg<D, 208>::kSmem;
+    case 224: return FCfg<D, 224>::kSmem;
+    case 240: return FCfg<D, 240>::kSmem;
+    case 256: return FCfg<D, 256>::kSmem;
+  }
+  return 0;
+}
+
+bool flat_disabled() {
+  static const bool off = [] {
+    const char* e = getenv("FWA_NO_FLAT");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
+}  // namespace
+
+bool tc_fwd_flat_supported(const Geom& g, int dtype, bool has_bias, bool has_mask) {
+  if (flat_disabled() || has_bias || has_mask) return false;
+  if (dtype != FWA_F16 && dtype != FWA_BF16) return false;
+  if (g.L <= 64 || g.L > 256 || g.L % 16 != 0) return false;
+  if (g.units * (int64_t)g.L >= ((int64_t)1 << 31)) return false;
+  switch (g.d) {
+    case 16: return fits_d<16>(g.L);
+    case 32: return fits_d<32>(g.L);
+    case 64: return fits_d<64>(g.L);
+  }
+  return false;
+}
+
+size_t tc_fwd_flat_smem(const Geom& g) {
+  switch (g.d) {
+    case 16: return smem_d<16>(g.L);
+    case 32: return smem_d<32>(g.L);
+    case 64: return smem_d<64>(g.L);
+  }
+  return 0;
+}
+
+int launch_fwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                       void* o, cudaStream_t s) {
+  const bool bf = dtype == FWA_BF16;
+  switch (g.d) {
+    case 16: return bf ? flat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, o, s)
+                       : flat_l<__half, 16>(g, dtype, q, k, v, o, s);
+    case 32: return bf ? flat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, o, s)
+                       : flat_l<__half, 32>(g, dtype, q, k, v, o, s);
+    case 64: return bf ? flat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, o, s)
+                       : flat_l<__half, 64>(g, dtype, q, k, v, o, s);
+  }
+  return fail(FWA_ERR_CAPACITY, "flat forward: unsupported head_dim");
+}
+
+}  // namespace fwa

@@ -605,6 +605,7 @@ bool tc_fwd_large_supported(const Geom& g, int dtype, bool has_bias, bool has_ma
 }
 
 size_t tc_fwd_large_smem(const Geom& g) {
+  if (tc_fwd_flat_supported(g, FWA_F16, false, false)) return tc_fwd_flat_smem(g);
   const int lp = (g.L + 15) / 16 * 16;
   const int row = g.d * 2;
   const int kv = (lp * row + 1023) / 1024 * 1024;
@@ -614,6 +615,8 @@ size_t tc_fwd_large_smem(const Geom& g) {
 
 int launch_fwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                         void* o, cudaStream_t s) {
+  if (tc_fwd_flat_supported(g, dtype, false, false))
+    return launch_fwd_tc_flat(g, dtype, q, k, v, o, s);
   const bool bf = dtype == FWA_BF16;
   switch (g.d) {
     case 16: return bf ? large_dispatch_l<__nv_bfloat16, 16>(g, dtype, q, k, v, o, s)

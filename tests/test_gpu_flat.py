@@ -1,0 +1,51 @@
+"""Flat-row large-window kernels (fwa_tc_flat.cu) on many units.
+
+The flat forward packs 128-row blocks across unit boundaries and gives each CTA a
+contiguous unit range, so the interesting cases are unit counts that leave ragged
+ranges (not a multiple of the SM count), blocks holding 2-3 units (L < 128 or
+L % 128 != 0) and the last, partial block of every range. Checked against a float32
+torch restatement of the oracle's math (oracle/flashwin_oracle.py: softmax(QK^T s) V)
+within the package's 16-bit tolerance.
+"""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+fwa = pytest.importorskip("paper_2501_06480_b200")
+ops = fwa.ops
+
+
+def _ref(q, k, v, scale):
+    s = (q.float() @ k.float().transpose(-1, -2)) * scale
+    return torch.softmax(s, -1) @ v.float()
+
+
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("units,L,d", [
+    (149, 144, 32), (301, 144, 32), (1000, 144, 32), (150, 80, 32), (151, 96, 16), (299, 112, 64),
+    (148, 128, 32), (297, 160, 32), (160, 192, 16), (149, 208, 32), (300, 240, 32), (151, 256, 32),
+    (149, 256, 64), (150, 144, 64), (7, 144, 32), (1, 256, 32),
+])
+def test_flat_forward_matches_fp32(dt, units, L, d):
+    rng = fwa.Rng(units * 31 + L + d)
+    shape = (units, 1, L, d)
+    q, k, v = (fwa.fill_uniform(rng, shape, dtype=dt) for _ in range(3))
+    scale = d ** -0.5
+    o = ops.attention_forward(q, k, v, scale)
+    ref = _ref(q, k, v, scale)
+    err = (o.float() - ref).abs().max().item()
+    assert err <= 2e-2, err
+    assert torch.isfinite(o).all()
+    assert fwa._native.device_flags() == 0
+
+
+def test_flat_forward_heads_layout_is_flat_over_units():
+    # (N, h) units are contiguous in [N][h][L][d]: heads change nothing for the flat kernel
+    rng = fwa.Rng(5)
+    q, k, v = (fwa.fill_uniform(rng, (37, 4, 144, 32), dtype=torch.float16) for _ in range(3))
+    o = ops.attention_forward(q, k, v, 0.2)
+    o_flat = ops.attention_forward(q.view(148, 1, 144, 32), k.view(148, 1, 144, 32),
+                                   v.view(148, 1, 144, 32), 0.2)
+    assert torch.equal(o.view(148, 1, 144, 32), o_flat)
