@@ -142,6 +142,12 @@ size_t tc_bwd_large_smem(const Geom& g);
 int launch_bwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                         const void* dout, void* dq, void* dk, void* dv, cudaStream_t s);
 
+// flat-row backward (fwa_tc_flat_bwd.cu); taken by launch_bwd_tc_large when supported
+bool tc_bwd_flat_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias);
+size_t tc_bwd_flat_smem(const Geom& g);
+int launch_bwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                       const void* dout, void* dq, void* dk, void* dv, cudaStream_t s);
+
 int device_sm_count();
 int64_t device_l2_bytes();
 size_t device_max_smem_optin();

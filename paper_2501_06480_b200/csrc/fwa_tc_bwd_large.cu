@@ -491,6 +491,7 @@ int bwd_large_l(const Geom& g, int dtype, const void* q, const void* k, const vo
 }  // namespace
 
 bool tc_bwd_large_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias) {
+  if (tc_bwd_flat_supported(g, dtype, has_bias, has_mask, want_dbias)) return true;
   if (has_bias || has_mask || want_dbias) return false;
   if (dtype != FWA_F16 && dtype != FWA_BF16) return false;
   if (g.L <= 64 || g.L > 256) return false;
@@ -501,6 +502,7 @@ bool tc_bwd_large_supported(const Geom& g, int dtype, bool has_bias, bool has_ma
 }
 
 size_t tc_bwd_large_smem(const Geom& g) {
+  if (tc_bwd_flat_supported(g, FWA_F16, false, false, false)) return tc_bwd_flat_smem(g);
   const int lp = (g.L + 15) / 16 * 16;
   const int row = g.d * 2;
   const int slot = (lp * row + 1023) / 1024 * 1024;
@@ -511,6 +513,8 @@ size_t tc_bwd_large_smem(const Geom& g) {
 
 int launch_bwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                         const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
+  if (tc_bwd_flat_supported(g, dtype, false, false, false))
+    return launch_bwd_tc_flat(g, dtype, q, k, v, dout, dq, dk, dv, s);
   const bool bf = dtype == FWA_BF16;
   switch (g.d) {
     case 16: return bf ? bwd_large_l<__nv_bfloat16, 16>(g, dtype, q, k, v, dout, dq, dk, dv, s)

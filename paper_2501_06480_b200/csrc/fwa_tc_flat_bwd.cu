@@ -1,0 +1,742 @@
+// fwa_tc_flat_bwd.cu — "flat-row" backward for large windows (64 < L <= 256, L % 16 == 0,
+// 2L + (2*ceil(L/128)+1)*d <= 512 TMEM columns; e.g. Swin-B 12x12: L = 144, d = 32) on
+// tcgen05 + TMA (sm_100a), f16/bf16, no bias/mask.
+//
+// As in fwa_tc_flat.cu the CTA owns a contiguous unit range and walks its flat
+// [units*L][d] rows in 128-row query blocks that straddle unit boundaries, so every
+// TMEM lane / softmax thread carries a real query row. Per block b (segments = the
+// units it intersects, lane-masked MMAs per segment):
+//
+//   S  = Q_b K_u^T, dP = dO_b V_u^T          TMEM [0, L), [L, 2L)      (SS, N = L)
+//   softmax warps (8: two per lane quarter, each owns half of the row's keys; row
+//   max / sum / rho combined through smem):
+//     p = 2^(S*c - m*c) (unnormalized)        -> smem sP (f16/bf16, SW128 K-major atoms)
+//     dO_b rows scaled by 1/l in place        (so dV += p^T (dO/l) = P^T dO)
+//     rho = sum_j p dP / l, dS = (scale/l) p (dP - rho) -> smem sDS
+//   dV_u += p^T dO'_b, dK_u += dS^T Q_b        M = keys (A read MN-major from sP/sDS),
+//                                              K = the segment's query rows, TMEM accumulators
+//   dQ_b  = dS K_u                             (SS, masked per segment) -> TMEM
+//   4 drain warps: dQ_b per block; dK_u / dV_u when unit u's last rows are done.
+//
+// The MMA warp issues S(b+1), dP(b+1) before the gradient MMAs of block b, so the softmax
+// of b+1 overlaps them. One dK/dV accumulator set: a block that finishes unit u and starts
+// u+1 issues u's gradients, commits them for draining, issues dQ_b (covering the drain) and
+// only then starts u+1. HBM: Q, K, V, dO read once; dQ, dK, dV written once (7 L d per unit).
+#include <cuda.h>
+#include <math.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <numeric>
+
+#include "fwa_common.cuh"
+#include "fwa_sm100.cuh"
+
+#ifdef FWA_TRACE
+__device__ long long g_bflat_trace[16][64];
+extern "C" int fwa_bflat_trace_copy(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_bflat_trace, sizeof(g_bflat_trace));
+}
+#define BTRACE(ev, b)                                                   \
+  do {                                                                  \
+    if (blockIdx.x == 0 && (b) < 64) g_bflat_trace[ev][b] = clock64();  \
+  } while (0)
+#else
+#define BTRACE(ev, b) \
+  do {                \
+  } while (0)
+#endif
+
+namespace fwa {
+namespace {
+
+using namespace sm100;
+
+constexpr int kBThreads = 448;  // producer, MMA, 8 softmax warps, 4 drain warps
+constexpr int kRows = 128;
+
+__host__ __device__ constexpr int span_units(int L, int rows) {
+  return (L - std::gcd(128, L) + rows + L - 1) / L;
+}
+
+template <int D, int L>
+struct BFCfg {
+  static constexpr int kRowBytes = D * 2;
+  static constexpr int kTile = kRows * kRowBytes;        // one 128-row Q or dO block
+  static constexpr int kNKT = (L + 127) / 128;           // 128-key tiles (M of dK/dV)
+  static constexpr int kAtoms = (L + 63) / 64;           // 64-key SW128 atom columns
+  static constexpr int kPBytes = kAtoms * 16384;         // sP / sDS: [128 rows][64 keys] atoms
+  static constexpr int kKVBytes = L * kRowBytes;
+  static constexpr int kKVSlot = (kKVBytes + 1023) / 1024 * 1024;
+  static constexpr int kQS = 2;                          // Q/dO block stages
+  static constexpr int kFixed = 1024 + 2 * kPBytes + kQS * 2 * kTile + kTile + 4096;
+  static constexpr int kKVAvail = (227 * 1024 - kFixed) / (2 * kKVSlot);
+  static constexpr int kKS = kKVAvail < 6 ? kKVAvail : 6;
+  static constexpr int kSmem = kFixed + kKS * 2 * kKVSlot;
+  static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
+  static constexpr int kChunks = kRowBytes / 16;
+  // TMEM columns: S, dP, dQ, dV (two sets, by unit parity, when they fit), dK
+  static constexpr bool kDV2 = 2 * L + D + 3 * kNKT * D <= 512;
+  static constexpr int kVSets = kDV2 ? 2 : 1;
+  static constexpr uint32_t kTS = 0, kTDP = L, kTDQ = 2 * L;
+  static constexpr uint32_t kTDV = 2 * L + D, kTDK = 2 * L + D + kVSets * kNKT * D;
+  static constexpr int kCols = 2 * L + D + (kVSets + 1) * kNKT * D;
+  // units touched between the oldest block with pending gradients and the newest S
+  static constexpr int kNeedKV = span_units(L, 2 * kRows);
+  // the MN-major dK/dV reads of key tile kt span atoms [2kt, 2kt+2): the last one may run
+  // past sP's kAtoms (into sDS) or past sDS (into the Q/dO ring) -- in bounds, garbage
+  // keys feed only lanes >= L, which are never stored.
+  static constexpr bool kFits = (L % 16 == 0) && kCols <= 512 && kKS >= kNeedKV &&
+                                kSmem <= 227 * 1024 && 2 * kNKT - kAtoms <= 1;
+};
+
+struct BFBarriers {
+  uint64_t qd_full[2], qd_empty[2], kv_full[6], kv_empty[6];
+  uint64_t s_full, dp_full, p_ready, ds_ready, p_free, ds_free;
+  uint64_t acc_full, acc_free, dq_full, dq_free;
+  uint32_t tmem_base;
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t bpack2(float a, float b) {
+  if constexpr (DT<T>::id == FWA_BF16) {
+    __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h2);
+  } else {
+    __half2 h2 = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h2);
+  }
+}
+template <typename T>
+__device__ __forceinline__ float2 bunpack2(uint32_t w) {
+  if constexpr (DT<T>::id == FWA_BF16) {
+    return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
+  } else {
+    return __half22float2(*reinterpret_cast<const __half2*>(&w));
+  }
+}
+
+__device__ __forceinline__ float bfmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// disable-output-lane word w: bit set = lane outside [lo, hi)
+__device__ __forceinline__ uint32_t blane_off(int w, int lo, int hi) {
+  const int a = max(lo - 32 * w, 0), b = min(hi - 32 * w, 32);
+  if (b <= a) return 0xffffffffu;
+  const uint32_t in = (b - a == 32) ? 0xffffffffu : (((1u << (b - a)) - 1u) << a);
+  return ~in;
+}
+
+// byte offset of (row r, 8-key chunk c of atom column a) in a [128][keys] SW128 K-major tile
+__device__ __forceinline__ int patom_off(int a, int r, int c) {
+  return a * 16384 + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
+}
+
+// TMEM load of N (multiple of 8) consecutive columns into v[0..N); the start column is
+// OFF (0 or 8) mod 16, so .x16 loads stay 16-column aligned
+template <int N, int OFF>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* v) {
+  static_assert(N % 8 == 0 && (OFF == 0 || OFF == 8), "8-column granularity");
+  constexpr int c0 = OFF == 8 ? 8 : 0;
+  if constexpr (OFF == 8) tmem_ld8(taddr, v);
+#pragma unroll
+  for (int c = c0; c + 16 <= N; c += 16) tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v + c));
+  if constexpr ((N - c0) % 16 == 8) tmem_ld8(taddr + (N - 8), v + (N - 8));
+}
+
+// Streams N (multiple of 8) columns in 8-column pieces, the next piece's tcgen05.ld in
+// flight while f(piece index, values) runs on the current one.
+template <int N, typename F>
+__device__ __forceinline__ void tmem_stream(uint32_t taddr, F&& f) {
+  uint32_t buf[2][8];
+  tmem_ld8(taddr, buf[0]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int c = 0; c < N / 8; ++c) {
+    if (c + 1 < N / 8) tmem_ld8(taddr + (c + 1) * 8, buf[(c + 1) & 1]);
+    f(c, buf[c & 1]);
+    tmem_wait_ld();
+  }
+}
+
+template <typename T, int D, int L>
+__global__ void __launch_bounds__(kBThreads, 1)
+bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dq16,
+                const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dk16,
+                const __grid_constant__ CUtensorMap tm_dv, const __grid_constant__ CUtensorMap tm_dv16,
+                int64_t n_units, float scale) {
+  using C = BFCfg<D, L>;
+  constexpr bool kBF16 = DT<T>::id == FWA_BF16;
+  constexpr int QS = C::kQS, KS = C::kKS, NKT = C::kNKT;
+  constexpr int H = L / 2;  // keys per softmax thread (one half of the row)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sP = smem;
+  uint8_t* sDS = sP + C::kPBytes;
+  uint8_t* sQD = sDS + C::kPBytes;                   // [QS][Q | dO] blocks
+  uint8_t* sK = sQD + QS * 2 * C::kTile;             // [KS] K slots
+  uint8_t* sV = sK + KS * C::kKVSlot;                // [KS] V slots
+  uint8_t* sSt = sV + KS * C::kKVSlot;               // dQ / dK / dV store staging
+  float* red = reinterpret_cast<float*>(sSt + C::kTile);    // [3][2][128] row partials
+  BFBarriers* bars = reinterpret_cast<BFBarriers*>(red + 3 * 2 * 128);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  const int64_t ua = (int64_t)blockIdx.x * n_units / gridDim.x;
+  const int64_t ub = (int64_t)(blockIdx.x + 1) * n_units / gridDim.x;
+  const int r0 = (int)(ua * L), r1 = (int)(ub * L);
+  const int nblk = (r1 - r0 + kRows - 1) / kRows;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < QS; ++s) {
+      mbar_init(&bars->qd_full[s], 1);
+      mbar_init(&bars->qd_empty[s], 1);
+    }
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(&bars->kv_full[s], 1);
+      mbar_init(&bars->kv_empty[s], 1);
+    }
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->dp_full, 1);
+    mbar_init(&bars->p_ready, 256);
+    mbar_init(&bars->ds_ready, 256);
+    mbar_init(&bars->p_free, 1);
+    mbar_init(&bars->ds_free, 1);
+    mbar_init(&bars->acc_full, 1);
+    mbar_init(&bars->acc_free, 128);
+    mbar_init(&bars->dq_full, 1);
+    mbar_init(&bars->dq_free, 128);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_do);
+  }
+  if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+  griddep_launch_dependents();
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0 && nblk > 0) {
+      griddep_wait();
+      const uint64_t pol = policy_evict_first();
+      const int n_loc = (int)(ub - ua);
+      int next = 0;
+      for (int b = 0; b < nblk; ++b) {
+        const int rs = r0 + b * kRows;
+        const int last = (min(rs + kRows, r1) - 1) / L - (int)ua;
+        for (; next <= last && next < n_loc; ++next) {
+          const int s = next % KS;
+          mbar_wait(&bars->kv_empty[s], ((next / KS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bars->kv_full[s], 2 * C::kKVBytes);
+          const int row = (int)((ua + next) * L);
+          tma_load_3d(sK + s * C::kKVSlot, &tm_k, &bars->kv_full[s], 0, row, 0, pol);
+          tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->kv_full[s], 0, row, 0, pol);
+        }
+        const int qs = b % QS;
+        mbar_wait(&bars->qd_empty[qs], ((b / QS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->qd_full[qs], 2 * C::kTile);
+        tma_load_3d(sQD + qs * 2 * C::kTile, &tm_q, &bars->qd_full[qs], 0, rs, 0, pol);
+        tma_load_3d(sQD + qs * 2 * C::kTile + C::kTile, &tm_do, &bars->qd_full[qs], 0, rs, 0, pol);
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer: S(b), dP(b), then the gradients of block b-1 =====
+    if (nblk > 0) {
+      constexpr uint32_t idS = make_idesc_f16(kBF16, 128, L, false, false);
+      constexpr uint32_t idMN = make_idesc_f16(kBF16, 128, D, true, true);   // dV, dK
+      constexpr uint32_t idQ = make_idesc_f16(kBF16, 128, D, false, true);   // dQ
+      constexpr uint32_t sbo = 8 * C::kRowBytes;
+      const uint32_t p0 = smem_u32(sP), ds0 = smem_u32(sDS);
+      int n_done = 0;  // units whose dK/dV were committed for draining
+      auto kslot = [&](int u) { return (u - (int)ua) % KS; };
+      auto issue_SdP = [&](int b) {
+        const int qs = b % QS;
+        const int rs = r0 + b * kRows, re = min(rs + kRows, r1);
+        const int u0 = rs / L, u1 = (re - 1) / L;
+        mbar_wait(&bars->qd_full[qs], (b / QS) & 1);
+        for (int u = u0; u <= u1; ++u) {
+          const int lu = u - (int)ua;
+          mbar_wait(&bars->kv_full[lu % KS], (lu / KS) & 1);
+        }
+        if (b > 0) mbar_wait(&bars->ds_ready, (b - 1) & 1);   // S / dP of b-1 consumed
+        tc_fence_after();
+        if (lane == 0) BTRACE(0, b);
+        const uint32_t q0 = smem_u32(sQD + qs * 2 * C::kTile), do0 = q0 + C::kTile;
+        for (int u = u0; u <= u1; ++u) {
+          const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
+          const uint32_t m0 = blane_off(0, lo, hi), m1 = blane_off(1, lo, hi);
+          const uint32_t m2 = blane_off(2, lo, hi), m3 = blane_off(3, lo, hi);
+          const uint64_t a_q = make_sdesc(q0, 16, sbo, C::kSwz);
+          const uint64_t b_k = make_sdesc(smem_u32(sK + kslot(u) * C::kKVSlot), 16, sbo, C::kSwz);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_f16_ss_m(tmem + C::kTS, a_q + ((kk * 32) >> 4), b_k + ((kk * 32) >> 4), idS, kk > 0,
+                           m0, m1, m2, m3);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit(&bars->s_full);
+        __syncwarp();
+        for (int u = u0; u <= u1; ++u) {
+          const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
+          const uint32_t m0 = blane_off(0, lo, hi), m1 = blane_off(1, lo, hi);
+          const uint32_t m2 = blane_off(2, lo, hi), m3 = blane_off(3, lo, hi);
+          const uint64_t a_do = make_sdesc(do0, 16, sbo, C::kSwz);
+          const uint64_t b_v = make_sdesc(smem_u32(sV + kslot(u) * C::kKVSlot), 16, sbo, C::kSwz);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_f16_ss_m(tmem + C::kTDP, a_do + ((kk * 32) >> 4), b_v + ((kk * 32) >> 4), idS, kk > 0,
+                           m0, m1, m2, m3);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit(&bars->dp_full);
+        __syncwarp();
+      };
+      auto issue_dQ = [&](int c) {
+        const int rs = r0 + c * kRows, re = min(rs + kRows, r1);
+        const int u0 = rs / L, u1 = (re - 1) / L;
+        if (c > 0) mbar_wait(&bars->dq_free, (c - 1) & 1);   // dQ(c-1) pulled out of TMEM
+        tc_fence_after();
+        for (int u = u0; u <= u1; ++u) {
+          const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
+          const uint32_t m0 = blane_off(0, lo, hi), m1 = blane_off(1, lo, hi);
+          const uint32_t m2 = blane_off(2, lo, hi), m3 = blane_off(3, lo, hi);
+          const uint64_t a_ds = make_sdesc(ds0, 16, 1024, 2);
+          const uint64_t b_k = make_sdesc(smem_u32(sK + kslot(u) * C::kKVSlot), C::kKVSlot, sbo, C::kSwz);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < L / 16; ++kk)
+              mma_f16_ss_m(tmem + C::kTDQ, a_ds + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4),
+                           b_k + ((kk * 16 * C::kRowBytes) >> 4), idQ, kk > 0, m0, m1, m2, m3);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit(&bars->dq_full);
+        __syncwarp();
+      };
+      auto issue_grads = [&](int c) {
+        const int qs = c % QS;
+        const int rs = r0 + c * kRows, re = min(rs + kRows, r1);
+        const int u0 = rs / L, u1 = (re - 1) / L;
+        mbar_wait(&bars->p_ready, c & 1);
+        mbar_wait(&bars->ds_ready, c & 1);
+        tc_fence_after();
+        if (lane == 0) BTRACE(1, c);
+        const uint32_t q0 = smem_u32(sQD + qs * 2 * C::kTile), do0 = q0 + C::kTile;
+        const uint64_t a_p = make_sdesc(p0, 16384, 1024, 2), a_ds = make_sdesc(ds0, 16384, 1024, 2);
+        const uint64_t b_do = make_sdesc(do0, C::kTile, sbo, C::kSwz);
+        const uint64_t b_q = make_sdesc(q0, C::kTile, sbo, C::kSwz);
+        // dV_kt(+)= p^T dO' / dK_kt(+)= dS^T Q over the segment's 16-row query steps
+        auto mma_dv = [&](uint32_t col, int k_lo, int k_hi, int first) {
+          if (elect_one()) {
+#pragma unroll
+            for (int kt = 0; kt < NKT; ++kt)
+#pragma unroll
+              for (int kk = 0; kk < kRows / 16; ++kk)
+                if (kk >= k_lo && kk < k_hi)
+                  mma_f16_ss(tmem + col + kt * D, a_p + ((kt * 2 * 16384 + kk * 2048) >> 4),
+                             b_do + ((kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
+          }
+          __syncwarp();
+        };
+        auto mma_dk = [&](int k_lo, int k_hi, int first) {
+          if (elect_one()) {
+#pragma unroll
+            for (int kt = 0; kt < NKT; ++kt)
+#pragma unroll
+              for (int kk = 0; kk < kRows / 16; ++kk)
+                if (kk >= k_lo && kk < k_hi)
+                  mma_f16_ss(tmem + C::kTDK + kt * D, a_ds + ((kt * 2 * 16384 + kk * 2048) >> 4),
+                             b_q + ((kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
+          }
+          __syncwarp();
+        };
+        if constexpr (C::kDV2) {
+          // all dV first (a unit's two dV sets alternate by parity, no drain wait), so the
+          // softmax of c+1 may overwrite sP as early as possible
+          for (int u = u0; u <= u1; ++u) {
+            const int g_lo = max(u * L, rs), g_hi = min((u + 1) * L, re);
+            const int k_lo = (g_lo - rs) / 16, k_hi = (g_hi - rs) / 16;
+            mma_dv(C::kTDV + ((u - (int)ua) & 1) * NKT * D, k_lo, k_hi, g_lo == u * L ? k_lo : -1);
+          }
+          if (elect_one()) mma_commit(&bars->p_free);
+          __syncwarp();
+          if (lane == 0) BTRACE(8, c);
+        }
+        bool dq_issued = false;
+        for (int u = u0; u <= u1; ++u) {
+          const int g_lo = max(u * L, rs), g_hi = min((u + 1) * L, re);   // global rows
+          const bool starts = g_lo == u * L, ends = g_hi == (u + 1) * L;
+          if (starts && n_done > 0) {   // dK (and single-set dV) of the previous unit drained?
+            if (lane == 0 && u > u0) BTRACE(11, c);
+            mbar_wait(&bars->acc_free, (n_done - 1) & 1);
+            tc_fence_after();
+            if (lane == 0 && u > u0) BTRACE(12, c);
+          }
+          const int k_lo = (g_lo - rs) / 16, k_hi = (g_hi - rs) / 16;   // 16-row query steps
+          const int first = starts ? k_lo : -1;
+          if constexpr (!C::kDV2) mma_dv(C::kTDV, k_lo, k_hi, first);
+          mma_dk(k_lo, k_hi, first);
+          if (lane == 0) BTRACE(u == u0 ? 9 : 13, c);
+          if (ends) {
+            if (elect_one()) mma_commit(&bars->acc_full);
+            __syncwarp();
+            ++n_done;
+          }
+          if (!dq_issued) {   // dQ right after the first segment: covers the drain of its unit
+            issue_dQ(c);
+            dq_issued = true;
+            if (lane == 0) BTRACE(10, c);
+          }
+        }
+        // block c's P / dS / Q / dO fully read; release its units whose last rows were here
+        const int nxt_u0 = (c + 1 < nblk) ? (rs + kRows) / L : u1 + 1;
+        if (elect_one()) {
+          if constexpr (!C::kDV2) mma_commit(&bars->p_free);
+          mma_commit(&bars->ds_free);
+          mma_commit(&bars->qd_empty[qs]);
+          for (int u = u0; u <= u1 && u < nxt_u0; ++u) mma_commit(&bars->kv_empty[kslot(u)]);
+        }
+        __syncwarp();
+        if (lane == 0) BTRACE(2, c);
+      };
+      for (int b = 0; b < nblk; ++b) {
+        issue_SdP(b);
+        if (b > 0) issue_grads(b - 1);
+      }
+      issue_grads(nblk - 1);
+    }
+  } else if (warp < 10) {
+    // ===== softmax / dS: warp pair (w, w+4) share a lane quarter, each owns half the keys =====
+    const int hf = (warp - 2) >> 2;
+    const int qd = warp & 3;
+    const int r = qd * 32 + lane;
+    const uint32_t t_lane = (uint32_t)(qd * 32) << 16;
+    const float sl2 = scale * 1.4426950408889634f;
+    float* rmax = red;
+    float* rsum = red + 256;
+    float* rrho = red + 512;
+    const uint32_t ts = tmem + t_lane + C::kTS + hf * H;
+    const uint32_t tdp = tmem + t_lane + C::kTDP + hf * H;
+    uint32_t pk[H / 2];   // this half row of p (then dS) as 16-bit pairs
+    for (int b = 0; b < nblk; ++b) {
+      const int qs = b % QS;
+      mbar_wait(&bars->s_full, b & 1);
+      tc_fence_after();
+      const bool trc = warp == 4 && lane == 0;
+      if (trc) BTRACE(3, b);
+#ifdef FWA_TC_ONLY
+      // timing experiment: keep the barrier protocol, skip the math
+      if (b > 0) mbar_wait(&bars->p_free, (b - 1) & 1);
+      mbar_wait(&bars->dp_full, b & 1);
+      tc_fence_after();
+      mbar_arrive(&bars->p_ready);
+      tc_fence_before();
+      if (b > 0) mbar_wait(&bars->ds_free, (b - 1) & 1);
+      mbar_arrive(&bars->ds_ready);
+      continue;
+#endif
+      float mx = -INFINITY;
+      tmem_stream<H>(ts, [&](int c, const uint32_t* x) {   // S read 1: row max
+#pragma unroll
+        for (int t = 0; t < 8; t += 2) mx = bfmax3(mx, __uint_as_float(x[t]), __uint_as_float(x[t + 1]));
+      });
+      rmax[hf * 128 + r] = mx;
+      named_sync(1, 256);
+      mx = fmaxf(rmax[r], rmax[128 + r]);
+      const float mxs = mx * sl2;
+      float s0 = 0.f, s1 = 0.f;
+      tmem_stream<H>(ts, [&](int c, const uint32_t* x) {   // S read 2: p = 2^(s c - m c)
+#pragma unroll
+        for (int t = 0; t < 8; t += 2) {
+          const float a = ex2(fmaf(__uint_as_float(x[t]), sl2, -mxs));
+          const float e = ex2(fmaf(__uint_as_float(x[t + 1]), sl2, -mxs));
+          s0 += a;
+          s1 += e;
+          pk[c * 4 + (t >> 1)] = bpack2<T>(a, e);
+        }
+      });
+      rsum[hf * 128 + r] = s0 + s1;
+      // p -> sP once the gradient MMAs of b-1 stopped reading it
+      if (b > 0) mbar_wait(&bars->p_free, (b - 1) & 1);
+#pragma unroll
+      for (int c8 = 0; c8 < H / 8; ++c8) {
+        const int key = hf * H + c8 * 8;
+        *reinterpret_cast<uint4*>(sP + patom_off(key >> 6, r, (key & 63) >> 3)) =
+            make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+      }
+      if (trc) BTRACE(4, b);
+      named_sync(1, 256);
+      const float inv_l = __frcp_rn(rsum[r] + rsum[128 + r]);
+      // dO rows *= 1/l (after dP consumed dO): this half of the row's 16-byte chunks
+      mbar_wait(&bars->dp_full, b & 1);
+      tc_fence_after();
+      {
+        uint8_t* row = sQD + qs * 2 * C::kTile + C::kTile + r * C::kRowBytes;
+#pragma unroll
+        for (int c = hf * (C::kChunks / 2); c < (hf + 1) * (C::kChunks / 2); ++c) {
+          uint4 w = *reinterpret_cast<uint4*>(row + c * 16);
+          uint32_t* e = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 f = bunpack2<T>(e[t]);
+            e[t] = bpack2<T>(f.x * inv_l, f.y * inv_l);
+          }
+          *reinterpret_cast<uint4*>(row + c * 16) = w;
+        }
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&bars->p_ready);
+      if (trc) BTRACE(5, b);
+      float rho0 = 0.f, rho1 = 0.f;
+      tmem_stream<H>(tdp, [&](int c, const uint32_t* x) {   // dP read 1: sum_j p dP
+#pragma unroll
+        for (int t = 0; t < 8; t += 2) {
+          const float2 p = bunpack2<T>(pk[c * 4 + (t >> 1)]);
+          rho0 = fmaf(p.x, __uint_as_float(x[t]), rho0);
+          rho1 = fmaf(p.y, __uint_as_float(x[t + 1]), rho1);
+        }
+      });
+      rrho[hf * 128 + r] = rho0 + rho1;
+      named_sync(1, 256);
+      const float g = scale * inv_l;
+      const float rg = (rrho[r] + rrho[128 + r]) * inv_l * g;   // rho * scale / l
+      tmem_stream<H>(tdp, [&](int c, const uint32_t* x) {   // dP read 2: dS
+#pragma unroll
+        for (int t = 0; t < 8; t += 2) {
+          const float2 p = bunpack2<T>(pk[c * 4 + (t >> 1)]);
+          pk[c * 4 + (t >> 1)] = bpack2<T>(p.x * fmaf(__uint_as_float(x[t]), g, -rg),
+                                           p.y * fmaf(__uint_as_float(x[t + 1]), g, -rg));
+        }
+      });
+      tc_fence_before();   // S / dP reads done before ds_ready lets S(b+1) overwrite them
+      if (b > 0) mbar_wait(&bars->ds_free, (b - 1) & 1);
+#pragma unroll
+      for (int c8 = 0; c8 < H / 8; ++c8) {
+        const int key = hf * H + c8 * 8;
+        *reinterpret_cast<uint4*>(sDS + patom_off(key >> 6, r, (key & 63) >> 3)) =
+            make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&bars->ds_ready);
+      if (trc) BTRACE(6, b);
+    }
+  } else {
+    // ===== drain warps: dK/dV of finished units, dQ of every block =====
+    const int qd = warp & 3;
+    const int r = qd * 32 + lane;
+    const uint32_t t_lane = (uint32_t)(qd * 32) << 16;
+    const uint32_t oswz = (uint32_t)((r * C::kRowBytes) >> 7) & (C::kChunks - 1);
+    const bool leader = warp == 12 && lane == 0;
+    auto stage_row = [&](uint8_t* st, const uint32_t* x) {
+      uint8_t* row = st + r * C::kRowBytes;
+#pragma unroll
+      for (int c = 0; c < C::kChunks; ++c)
+        *reinterpret_cast<uint4*>(row + ((c ^ oswz) << 4)) = make_uint4(
+            bpack2<T>(__uint_as_float(x[8 * c]), __uint_as_float(x[8 * c + 1])),
+            bpack2<T>(__uint_as_float(x[8 * c + 2]), __uint_as_float(x[8 * c + 3])),
+            bpack2<T>(__uint_as_float(x[8 * c + 4]), __uint_as_float(x[8 * c + 5])),
+            bpack2<T>(__uint_as_float(x[8 * c + 6]), __uint_as_float(x[8 * c + 7])));
+    };
+    // one staging buffer: wait until the previous store has read it, fill, store
+    auto emit = [&](const uint32_t* x, const CUtensorMap* m128, const CUtensorMap* m16, int row0,
+                    int nrows) {
+      if (leader) bulk_wait_read<0>();
+      named_sync(2, 128);
+      stage_row(sSt, x);
+      fence_proxy_async_smem();
+      named_sync(3, 128);
+      if (leader) {
+        if (nrows == kRows) {
+          tma_store_3d(m128, sSt, 0, row0, 0);
+        } else {
+          for (int t = 0; t < nrows; t += 16) tma_store_3d(m16, sSt + t * C::kRowBytes, 0, row0 + t, 0);
+        }
+        bulk_commit();
+      }
+    };
+    int n_unit = 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int rs = r0 + b * kRows, re = min(rs + kRows, r1);
+      const int u0 = rs / L, u1 = (re - 1) / L;
+      for (int u = u0; u <= u1; ++u) {
+        if ((u + 1) * L > re) continue;   // unit continues into the next block
+        mbar_wait(&bars->acc_full, n_unit & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kt = 0; kt < NKT; ++kt) {
+          uint32_t gv[D], gk[D];
+#pragma unroll
+          for (int q = 0; q < D / 16; ++q) {
+            tmem_ld16(tmem + t_lane + C::kTDV + (C::kDV2 ? ((u - (int)ua) & 1) * NKT * D : 0) + kt * D + q * 16,
+                      *reinterpret_cast<uint32_t(*)[16]>(&gv[q * 16]));
+            tmem_ld16(tmem + t_lane + C::kTDK + kt * D + q * 16, *reinterpret_cast<uint32_t(*)[16]>(&gk[q * 16]));
+          }
+          tmem_wait_ld();
+          if (kt == NKT - 1) {
+            tc_fence_before();
+            mbar_arrive(&bars->acc_free);
+          }
+          const int nr = min(kRows, L - kt * kRows);
+          emit(gv, &tm_dv, &tm_dv16, u * L + kt * kRows, nr);
+          emit(gk, &tm_dk, &tm_dk16, u * L + kt * kRows, nr);
+        }
+        ++n_unit;
+      }
+      mbar_wait(&bars->dq_full, b & 1);
+      tc_fence_after();
+      uint32_t gq[D];
+#pragma unroll
+      for (int q = 0; q < D / 16; ++q)
+        tmem_ld16(tmem + t_lane + C::kTDQ + q * 16, *reinterpret_cast<uint32_t(*)[16]>(&gq[q * 16]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars->dq_free);
+      emit(gq, &tm_dq, &tm_dq16, rs, re - rs);
+      if (leader) BTRACE(7, b);
+    }
+    if (leader) bulk_wait_read<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+template <typename T, int D, int L>
+int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                   const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
+  using C = BFCfg<D, L>;
+  if constexpr (!C::kFits) {
+    return fail(FWA_ERR_CAPACITY, "flat backward: shape does not fit");
+  } else {
+    const int rows = (int)(g.units * L);
+    CUtensorMap m[10];
+    int rc;
+    if ((rc = get_units_map(&m[0], q, dtype, 1, rows, D, kRows, 1))) return rc;
+    if ((rc = get_units_map(&m[1], k, dtype, 1, rows, D, L, 1))) return rc;
+    if ((rc = get_units_map(&m[2], v, dtype, 1, rows, D, L, 1))) return rc;
+    if ((rc = get_units_map(&m[3], dout, dtype, 1, rows, D, kRows, 1))) return rc;
+    void* outs[3] = {dq, dk, dv};
+    for (int i = 0; i < 3; ++i) {
+      if ((rc = get_units_map(&m[4 + 2 * i], outs[i], dtype, 1, rows, D, kRows, 1))) return rc;
+      if ((rc = get_units_map(&m[5 + 2 * i], outs[i], dtype, 1, rows, D, 16, 1))) return rc;
+    }
+    auto kern = bwd_flat_kernel<T, D, L>;
+    static bool attr_done = false;
+    if (!attr_done) {
+      rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem),
+                      "cudaFuncSetAttribute(bwd_flat)");
+      if (rc) return rc;
+      attr_done = true;
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
+    rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kBThreads), (size_t)C::kSmem, s, m[0], m[1],
+                               m[2], m[3], m[4], m[5], m[6], m[7], m[8], m[9], (int64_t)g.units,
+                               g.scale),
+                    "bwd_flat_kernel launch");
+    if (rc) return rc;
+    count_launch();
+    return FWA_OK;
+  }
+}
+
+#define FWA_FLAT_LS(X) X(80) X(96) X(112) X(128) X(144) X(160) X(176) X(192) X(208) X(224) X(240) X(256)
+
+template <typename T, int D>
+int bflat_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, const void* dout,
+            void* dq, void* dk, void* dv, cudaStream_t s) {
+  switch (g.L) {
+#define FWA_CASE(LL) \
+  case LL: return launch_bflat_t<T, D, LL>(g, dtype, q, k, v, dout, dq, dk, dv, s);
+    FWA_FLAT_LS(FWA_CASE)
+#undef FWA_CASE
+  }
+  return fail(FWA_ERR_CAPACITY, "flat backward: unsupported L");
+}
+
+template <int D>
+constexpr bool bfits_d(int L) {
+  switch (L) {
+#define FWA_CASE(LL) \
+  case LL: return BFCfg<D, LL>::kFits;
+    FWA_FLAT_LS(FWA_CASE)
+#undef FWA_CASE
+  }
+  return false;
+}
+
+template <int D>
+constexpr int bsmem_d(int L) {
+  switch (L) {
+#define FWA_CASE(LL) \
+  case LL: return BFCfg<D, LL>::kSmem;
+    FWA_FLAT_LS(FWA_CASE)
+#undef FWA_CASE
+  }
+  return 0;
+}
+
+bool bflat_disabled() {
+  static const bool off = [] {
+    const char* e = getenv("FWA_NO_FLAT");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
+}  // namespace
+
+bool tc_bwd_flat_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias) {
+  if (bflat_disabled() || has_bias || has_mask || want_dbias) return false;
+  if (dtype != FWA_F16 && dtype != FWA_BF16) return false;
+  if (g.L <= 64 || g.L > 256 || g.L % 16 != 0) return false;
+  if (g.units * (int64_t)g.L >= ((int64_t)1 << 31)) return false;
+  switch (g.d) {
+    case 16: return bfits_d<16>(g.L);
+    case 32: return bfits_d<32>(g.L);
+    case 64: return bfits_d<64>(g.L);
+  }
+  return false;
+}
+
+size_t tc_bwd_flat_smem(const Geom& g) {
+  switch (g.d) {
+    case 16: return bsmem_d<16>(g.L);
+    case 32: return bsmem_d<32>(g.L);
+    case 64: return bsmem_d<64>(g.L);
+  }
+  return 0;
+}
+
+int launch_bwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                       const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
+  const bool bf = dtype == FWA_BF16;
+  switch (g.d) {
+    case 16: return bf ? bflat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, dout, dq, dk, dv, s)
+                       : bflat_l<__half, 16>(g, dtype, q, k, v, dout, dq, dk, dv, s);
+    case 32: return bf ? bflat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, dout, dq, dk, dv, s)
+                       : bflat_l<__half, 32>(g, dtype, q, k, v, dout, dq, dk, dv, s);
+    case 64: return bf ? bflat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, dout, dq, dk, dv, s)
+                       : bflat_l<__half, 64>(g, dtype, q, k, v, dout, dq, dk, dv, s);
+  }
+  return fail(FWA_ERR_CAPACITY, "flat backward: unsupported head_dim");
+}
+
+}  // namespace fwa

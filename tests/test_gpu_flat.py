@@ -49,3 +49,29 @@ def test_flat_forward_heads_layout_is_flat_over_units():
     o_flat = ops.attention_forward(q.view(148, 1, 144, 32), k.view(148, 1, 144, 32),
                                    v.view(148, 1, 144, 32), 0.2)
     assert torch.equal(o.view(148, 1, 144, 32), o_flat)
+
+
+def _ref_bwd(q, k, v, do, scale):
+    qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
+    o = torch.softmax((qf @ kf.transpose(-1, -2)) * scale, -1) @ vf
+    o.backward(do.float())
+    return qf.grad, kf.grad, vf.grad
+
+
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("units,L,d", [
+    (149, 144, 32), (301, 144, 32), (1000, 144, 32), (150, 80, 32), (151, 96, 16), (149, 112, 32),
+    (148, 128, 32), (297, 160, 32), (160, 176, 32), (149, 208, 16), (150, 128, 64), (7, 144, 32),
+    (1, 144, 32), (149, 256, 16),
+])
+def test_flat_backward_matches_fp32(dt, units, L, d):
+    rng = fwa.Rng(units * 17 + L + d)
+    shape = (units, 1, L, d)
+    q, k, v, do = (fwa.fill_uniform(rng, shape, dtype=dt) for _ in range(4))
+    scale = d ** -0.5
+    dq, dk, dv, _ = ops.attention_backward(q, k, v, do, scale)
+    for got, want in zip((dq, dk, dv), _ref_bwd(q, k, v, do, scale)):
+        err = (got.float() - want).abs().max().item()
+        assert err <= 2e-2, err
+        assert torch.isfinite(got).all()
+    assert fwa._native.device_flags() == 0
