@@ -180,6 +180,19 @@ __device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uin
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Predicated form (issued iff `issue` != 0): straight-line MMA sequences whose length
+// varies at run time without a branch per MMA (branches stop ptxas from overlapping the
+// per-MMA descriptor arithmetic of neighbouring MMAs).
+__device__ __forceinline__ void mma_f16_ss_p(uint32_t issue, uint32_t d_tmem, uint64_t a_desc,
+                                            uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(issue)
+      : "memory");
+}
 // D[tmem] (+)= A[tmem] * B[smem]; A is K-major in TMEM: lane = row, 32-bit column c holds
 // the 16-bit pair (k = 2c, 2c+1).
 __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
@@ -282,6 +295,14 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_byte
   d |= (uint64_t)1 << 46;  // version (sm_100)
   d |= (uint64_t)(layout & 7) << 61;
   return d;
+}
+
+// desc + off (16-byte units) computed right where it is used: keeps ptxas from hoisting a
+// table of per-MMA descriptors into vector registers (one R2UR per MMA on the issue path).
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t off16) {
+  uint64_t r;
+  asm volatile("add.s64 %0, %1, %2;" : "=l"(r) : "l"(d), "l"((uint64_t)off16));
+  return r;
 }
 
 // Instruction descriptor, kind::f16 with fp32 accumulate.

@@ -41,8 +41,24 @@ extern "C" int fwa_bflat_trace_copy(long long* host) {
   do {                                                                  \
     if (blockIdx.x == 0 && (b) < 64) g_bflat_trace[ev][b] = clock64();  \
   } while (0)
+#ifdef FWA_TC_ONLY
+// serialize: wait until every MMA issued so far has executed, then stamp event ev
+#define BPROBE(ev, b)                                   \
+  do {                                                  \
+    if (elect_one()) mma_commit(&bars->probe);          \
+    __syncwarp();                                       \
+    mbar_wait(&bars->probe, probe_ph);                  \
+    probe_ph ^= 1;                                      \
+    if (lane == 0) BTRACE(ev, b);                       \
+  } while (0)
+#endif
 #else
 #define BTRACE(ev, b) \
+  do {                \
+  } while (0)
+#endif
+#ifndef BPROBE
+#define BPROBE(ev, b) \
   do {                \
   } while (0)
 #endif
@@ -68,8 +84,13 @@ struct BFCfg {
   static constexpr int kPBytes = kAtoms * 16384;         // sP / sDS: [128 rows][64 keys] atoms
   static constexpr int kKVBytes = L * kRowBytes;
   static constexpr int kKVSlot = (kKVBytes + 1023) / 1024 * 1024;
-  static constexpr int kQS = 2;                          // Q/dO block stages
-  static constexpr int kFixed = 1024 + 2 * kPBytes + kQS * 2 * kTile + kTile + 4096;
+  static constexpr int kBase = 1024 + 2 * kPBytes + kTile + 4096;
+  // units touched between the oldest block with pending gradients and the newest S
+  static constexpr int kNeedKV = span_units(L, 2 * kRows);
+  // Q/dO stages: 3 when the K/V ring still holds kNeedKV + 1 units (K/V prefetch measured
+  // to matter more than a third Q/dO stage), else 2
+  static constexpr int kQS = (kBase + 3 * 2 * kTile + (kNeedKV + 1) * 2 * kKVSlot <= 227 * 1024) ? 3 : 2;
+  static constexpr int kFixed = kBase + kQS * 2 * kTile;
   static constexpr int kKVAvail = (227 * 1024 - kFixed) / (2 * kKVSlot);
   static constexpr int kKS = kKVAvail < 6 ? kKVAvail : 6;
   static constexpr int kSmem = kFixed + kKS * 2 * kKVSlot;
@@ -81,8 +102,6 @@ struct BFCfg {
   static constexpr uint32_t kTS = 0, kTDP = L, kTDQ = 2 * L;
   static constexpr uint32_t kTDV = 2 * L + D, kTDK = 2 * L + D + kVSets * kNKT * D;
   static constexpr int kCols = 2 * L + D + (kVSets + 1) * kNKT * D;
-  // units touched between the oldest block with pending gradients and the newest S
-  static constexpr int kNeedKV = span_units(L, 2 * kRows);
   // the MN-major dK/dV reads of key tile kt span atoms [2kt, 2kt+2): the last one may run
   // past sP's kAtoms (into sDS) or past sDS (into the Q/dO ring) -- in bounds, garbage
   // keys feed only lanes >= L, which are never stored.
@@ -91,9 +110,10 @@ struct BFCfg {
 };
 
 struct BFBarriers {
-  uint64_t qd_full[2], qd_empty[2], kv_full[6], kv_empty[6];
+  uint64_t qd_full[3], qd_empty[3], kv_full[6], kv_empty[6];
   uint64_t s_full, dp_full, p_ready, ds_ready, p_free, ds_free;
   uint64_t acc_full, acc_free, dq_full, dq_free;
+  uint64_t probe;
   uint32_t tmem_base;
 };
 
@@ -212,6 +232,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     mbar_init(&bars->acc_free, 128);
     mbar_init(&bars->dq_full, 1);
     mbar_init(&bars->dq_free, 128);
+    mbar_init(&bars->probe, 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -261,6 +282,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       constexpr uint32_t sbo = 8 * C::kRowBytes;
       const uint32_t p0 = smem_u32(sP), ds0 = smem_u32(sDS);
       int n_done = 0;  // units whose dK/dV were committed for draining
+      uint32_t probe_ph = 0;
+      (void)probe_ph;
       auto kslot = [&](int u) { return (u - (int)ua) % KS; };
       auto issue_SdP = [&](int b) {
         const int qs = b % QS;
@@ -307,6 +330,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         }
         if (elect_one()) mma_commit(&bars->dp_full);
         __syncwarp();
+        BPROBE(15, b);
       };
       auto issue_dQ = [&](int c) {
         const int rs = r0 + c * kRows, re = min(rs + kRows, r1);
@@ -322,8 +346,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < L / 16; ++kk)
-              mma_f16_ss_m(tmem + C::kTDQ, a_ds + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4),
-                           b_k + ((kk * 16 * C::kRowBytes) >> 4), idQ, kk > 0, m0, m1, m2, m3);
+              mma_f16_ss_m(tmem + C::kTDQ, desc_add(a_ds, ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4),
+                           desc_add(b_k, (kk * 16 * C::kRowBytes) >> 4), idQ, kk > 0, m0, m1, m2, m3);
           }
           __syncwarp();
         }
@@ -349,9 +373,9 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             for (int kt = 0; kt < NKT; ++kt)
 #pragma unroll
               for (int kk = 0; kk < kRows / 16; ++kk)
-                if (kk >= k_lo && kk < k_hi)
-                  mma_f16_ss(tmem + col + kt * D, a_p + ((kt * 2 * 16384 + kk * 2048) >> 4),
-                             b_do + ((kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
+                mma_f16_ss_p(kk >= k_lo && kk < k_hi, tmem + col + kt * D,
+                             desc_add(a_p, (kt * 2 * 16384 + kk * 2048) >> 4),
+                             desc_add(b_do, (kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
           }
           __syncwarp();
         };
@@ -361,9 +385,9 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             for (int kt = 0; kt < NKT; ++kt)
 #pragma unroll
               for (int kk = 0; kk < kRows / 16; ++kk)
-                if (kk >= k_lo && kk < k_hi)
-                  mma_f16_ss(tmem + C::kTDK + kt * D, a_ds + ((kt * 2 * 16384 + kk * 2048) >> 4),
-                             b_q + ((kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
+                mma_f16_ss_p(kk >= k_lo && kk < k_hi, tmem + C::kTDK + kt * D,
+                             desc_add(a_ds, (kt * 2 * 16384 + kk * 2048) >> 4),
+                             desc_add(b_q, (kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
           }
           __syncwarp();
         };
@@ -378,6 +402,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           if (elect_one()) mma_commit(&bars->p_free);
           __syncwarp();
           if (lane == 0) BTRACE(8, c);
+          BPROBE(4, c);
         }
         bool dq_issued = false;
         for (int u = u0; u <= u1; ++u) {
@@ -394,6 +419,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           if constexpr (!C::kDV2) mma_dv(C::kTDV, k_lo, k_hi, first);
           mma_dk(k_lo, k_hi, first);
           if (lane == 0) BTRACE(u == u0 ? 9 : 13, c);
+          BPROBE(u == u0 ? 5 : 7, c);
           if (ends) {
             if (elect_one()) mma_commit(&bars->acc_full);
             __syncwarp();
@@ -403,6 +429,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             issue_dQ(c);
             dq_issued = true;
             if (lane == 0) BTRACE(10, c);
+            BPROBE(6, c);
           }
         }
         // block c's P / dS / Q / dO fully read; release its units whose last rows were here
@@ -415,6 +442,10 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         }
         __syncwarp();
         if (lane == 0) BTRACE(2, c);
+#ifdef FWA_TC_ONLY
+        mbar_wait(&bars->ds_free, c & 1);   // timing experiment: when did the TC finish grads(c)?
+        if (lane == 0) BTRACE(14, c);
+#endif
       };
       for (int b = 0; b < nblk; ++b) {
         issue_SdP(b);

@@ -24,7 +24,7 @@ buf = (ctypes.c_longlong * (16 * 64))()
 assert lib.fwa_bflat_trace_copy(buf) == 0
 t = np.array(buf, dtype=np.int64).reshape(16, 64)
 t0 = t[0, 0]
-names = ["SdP_iss", "grad_beg", "grad_end", "sm_start", "p_stored", "p_ready", "ds_ready", "dq_out", "dV_done", "dK0_done", "dQ_done", "accw_beg", "accw_end", "dK1_done"]
+names = ["SdP_iss", "grad_beg", "grad_end", "sm_start", "p_stored", "p_ready", "ds_ready", "dq_out", "dV_done", "dK0_done", "dQ_done", "accw_beg", "accw_end", "dK1_done", "tc_done"]
 print("blk " + " ".join(f"{n:>9}" for n in names))
 for b in range(30):
-    print(f"{b:3d} " + " ".join(f"{(t[e, b] - t0) if t[e, b] else -1:9d}" for e in range(14)))
+    print(f"{b:3d} " + " ".join(f"{(t[e, b] - t0) if t[e, b] else -1:9d}" for e in range(15)))
