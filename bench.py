@@ -50,7 +50,7 @@ WORKLOADS = {
     "swin_b_fwdbwd": dict(layers=SWIN_B384, batch=64, dtype="float16", bwd=True, extras=False,
                           k=12, desc="Swin-B 384^2 window 12 B=64, fp16 forward+backward "
                                      "(configs[3])"),
-    "large_sweep": dict(layers=LARGE, batch=1, dtype="float16", bwd=False, extras=False, k=8,
+    "large_sweep": dict(layers=LARGE, batch=1, cpu_div=512, dtype="float16", bwd=False, extras=False, k=8,
                         desc="large-window sweep L=64/256, d=32/64, ~1 GB per call, fp16 "
                              "forward (configs[4])"),
 }
@@ -158,18 +158,23 @@ def cpu_reference(wl, seconds_target=12.0, steps=1, warmup=0):
     os.environ["OMP_NUM_THREADS"] = "1"
     cores = len(os.sched_getaffinity(0))
     layers = wl["layers"]
-    _, t = _cpu_worker((layers, wl["batch"], 1, wl["bwd"], 1))
+    # one CPU sample "image" = N / cpu_div windows of every layer (cpu_div defaults to the
+    # batch: one real image; the large sweep has no images, 1/512 of each ~1 GB call)
+    div = wl.get("cpu_div", wl["batch"])
+    _, t = _cpu_worker((layers, div, 1, wl["bwd"], 1))
     per_proc = max(1, int(seconds_target / max(t, 1e-3) / max(steps + warmup, 1)))
     results = []
-    with mp.get_context("fork").Pool(cores) as pool:
+    # spawn, not fork: the parent holds a CUDA context (forking it can hang the children)
+    with mp.get_context("spawn").Pool(cores) as pool:
         for s in range(warmup + steps):
-            outs = pool.map(_cpu_worker, [(layers, wl["batch"], per_proc, wl["bwd"], 100 + i)
+            outs = pool.map(_cpu_worker, [(layers, div, per_proc, wl["bwd"], 100 + i)
                                           for i in range(cores)])
             if s >= warmup:
                 results.append((sum(o[0] for o in outs), max(o[1] for o in outs)))
     windows = sum(r[0] for r in results)
     secs = sum(r[1] for r in results)
-    sample = (f"{per_proc} image(s) x {cores} processes per step through all {len(layers)} "
+    unit = "image(s)" if div == wl["batch"] else f"1/{div}-of-call slice(s)"
+    sample = (f"{per_proc} {unit} x {cores} processes per step through all {len(layers)} "
               f"layers, float64 oracle port of flash.py Alg.1{'/2' if wl['bwd'] else ''} "
               f"(numpy, 1 BLAS thread per process; windows/s = windows / slowest process time)")
     return windows / secs, cores, sample, secs / max(len(results), 1)
