@@ -317,6 +317,21 @@ __host__ __device__ constexpr uint32_t make_idesc_f16(bool bf16, int M, int N, b
          | ((uint32_t)(M >> 4) << 24);             // m_dim
 }
 
+// 2^x for x <= 0 on the FMA/ALU pipes (no MUFU): Cody-Waite split x = j + f, f in
+// [-0.5, 0.5], degree-3 fit of 2^f (max relative error 7.7e-5, below the 16-bit P
+// rounding), exponent added as an integer. Used for a share of the softmax exponentials
+// so the MUFU (16 ex2/clk/SM) is not the softmax bottleneck.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;          // 1.5 * 2^23: round-to-nearest integer in the low bits
+  const float j = t - 12582912.f;
+  const float f = x - j;
+  float p = fmaf(0.05508868396282196f, f, 0.24260404706001282f);
+  p = fmaf(p, f, 0.6932762265205383f);
+  p = fmaf(p, f, 0.9999289512634277f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -51,7 +51,8 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kFThreads = 320;  // producer, MMA, 2 x 4 softmax/epilogue warps
+// warps: 0 producer, 1 S issuer, 2..9 softmax (+ epilogue unless split), 10 PV issuer,
+// 11..14 epilogue (split mode)
 constexpr int kRows = 128;
 
 // units intersecting one 128-row block: block starts are multiples of gcd(128, L) inside
@@ -67,7 +68,7 @@ struct FCfg {
   static constexpr int kKVBytes = L * kRowBytes;
   static constexpr int kKVSlot = (kKVBytes + 1023) / 1024 * 1024;
   static constexpr int kQStages = D >= 64 ? 2 : 4;
-  static constexpr int kFixed = 1024 + kQStages * kQBytes + 2 * kQBytes + 1024;
+  static constexpr int kFixed = 1024 + kQStages * kQBytes + 2 * kQBytes + 1536;   // + barriers, sInv
   static constexpr int kKVAvail = (227 * 1024 - kFixed) / (2 * kKVSlot);
   static constexpr int kKVStages = kKVAvail < 8 ? kKVAvail : 8;
   static constexpr int kSmem = kFixed + kKVStages * 2 * kKVSlot;
@@ -75,12 +76,24 @@ struct FCfg {
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
   static constexpr int kChunks = kRowBytes / 16;
   static constexpr uint32_t kOCol = ((L / 2 + 15) / 16) * 16;
-  static constexpr bool kFits = kKVStages >= 2 * kMaxSeg && kOCol + D <= 256 && kSmem <= 227 * 1024;
+  // TMEM buffer = S [0, L), then P over [0, L/2) and O at [kOCol, kOCol + D); three buffers
+  // when they fit in 512 columns (S of block b+2 is issued while b+1 and b are in flight)
+  static constexpr int kBW = ((L > (int)kOCol + D ? L : (int)kOCol + D) + 15) / 16 * 16;
+  // split mode (L up to ~150): two S slots [0, 2L) plus two P/O slots (P then O) of kPW
+  // columns. The S slot frees as soon as the softmax has read S, so S(b+2) runs while P(b)
+  // still waits for PV, and a separate epilogue warpgroup drains O.
+  static constexpr int kPW = (int)kOCol + D;
+  static constexpr bool kSplit = 2 * L + 2 * kPW <= 512;
+  static constexpr int kNB = kSplit ? 2 : (3 * kBW <= 512 ? 3 : 2);
+  static constexpr int kThreads = kSplit ? 480 : 352;
+  // units resident between the oldest block awaiting PV and the newest S
+  static constexpr int kNeedKV = (L - std::gcd(128, L) + (kNB + 1) * kRows + L - 1) / L;
+  static constexpr bool kFits = kKVStages >= kNeedKV && kBW <= 256 && kSmem <= 227 * 1024;
 };
 
 struct FBarriers {
   uint64_t q_full[4], q_empty[4], kv_full[8], kv_empty[8];
-  uint64_t s_full[2], p_ready[2], o_full[2], buf_free[2];
+  uint64_t s_full[3], p_ready[3], o_full[3], buf_free[3];
   uint32_t tmem_base;
 };
 
@@ -122,14 +135,34 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 
+// Streams one TMEM row segment [0, N) in 32-column pieces (the last may be 16 wide): the
+// next piece's tcgen05.ld is in flight while f(first column, values) runs on this one.
+template <int N, typename F>
+__device__ __forceinline__ void srow_stream(uint32_t taddr, F&& f) {
+  uint32_t buf[2][32];
+  constexpr int kPieces = (N + 31) / 32;
+  auto load = [&](int c, uint32_t (&r)[32]) {
+    if (c * 32 + 32 <= N) tmem_ld32(taddr + c * 32, r);
+    else tmem_ld16(taddr + c * 32, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+  };
+  load(0, buf[0]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int c = 0; c < kPieces; ++c) {
+    if (c + 1 < kPieces) load(c + 1, buf[(c + 1) & 1]);
+    f(c * 32, buf[c & 1]);
+    tmem_wait_ld();
+  }
+}
+
 template <typename T, int D, int L>
-__global__ void __launch_bounds__(kFThreads, 1)
+__global__ void __launch_bounds__(FCfg<D, L>::kThreads, 1)
 fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                 const __grid_constant__ CUtensorMap tm_o16, int64_t n_units, float scale_log2) {
   using C = FCfg<D, L>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
-  constexpr int QS = C::kQStages, KS = C::kKVStages;
+  constexpr int QS = C::kQStages, KS = C::kKVStages, NB = C::kNB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -156,7 +189,7 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       mbar_init(&bars->kv_full[s], 1);
       mbar_init(&bars->kv_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 3; ++s) {
       mbar_init(&bars->s_full[s], 1);
       mbar_init(&bars->p_ready[s], 128);
       mbar_init(&bars->o_full[s], 1);
@@ -176,6 +209,11 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  float* sInv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);   // [2][128]
+  // TMEM columns of block b: S, P (16-bit pairs), O
+  auto s_col = [&](int b) -> uint32_t { return C::kSplit ? (b & 1) * L : (b % NB) * C::kBW; };
+  auto p_col = [&](int b) -> uint32_t { return C::kSplit ? 2 * L + (b & 1) * C::kPW : (b % NB) * C::kBW; };
+  auto o_col = [&](int b) -> uint32_t { return p_col(b) + C::kOCol; };
   griddep_launch_dependents();
 
   if (warp == 0) {
@@ -203,13 +241,12 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer (whole warp runs the control flow, one elected lane issues) =====
+    // ===== S issuer: S(b) into TMEM buffer b % NB as soon as its inputs and buffer are ready =====
     if (nblk > 0) {
       constexpr uint32_t idS = make_idesc_f16(kBF16, 128, L, false, false);
-      constexpr uint32_t idO = make_idesc_f16(kBF16, 128, D, false, true);
       constexpr uint32_t sbo = 8 * C::kRowBytes;
-      auto issue_S = [&](int b) {
-        const int j = b & 1, qs = b % QS;
+      for (int b = 0; b < nblk; ++b) {
+        const int j = b % NB, qs = b % QS;
         const int rs = r0 + b * kRows, re = min(rs + kRows, r1);
         const int u0 = rs / L, u1 = (re - 1) / L;
         mbar_wait(&bars->q_full[qs], (b / QS) & 1);
@@ -218,20 +255,25 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           mbar_wait(&bars->kv_full[lu % KS], (lu / KS) & 1);
         }
         FTRACE(0, b);
-        if (b >= 2) mbar_wait(&bars->buf_free[j], ((b >> 1) - 1) & 1);
+        if (C::kSplit) {
+          if (b >= 2) mbar_wait(&bars->p_ready[b & 1], ((b >> 1) - 1) & 1);   // S slot read
+        } else if (b >= NB) {
+          mbar_wait(&bars->buf_free[j], ((b / NB) - 1) & 1);
+        }
         tc_fence_after();
         FTRACE(1, b);
-        const uint32_t q0 = smem_u32(sQ + qs * C::kQBytes);
+        const uint64_t a_q = make_sdesc(smem_u32(sQ + qs * C::kQBytes), 16, sbo, C::kSwz);
         for (int u = u0; u <= u1; ++u) {
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
           const uint32_t m0 = lane_off(0, lo, hi), m1 = lane_off(1, lo, hi);
           const uint32_t m2 = lane_off(2, lo, hi), m3 = lane_off(3, lo, hi);
-          const uint32_t k0 = smem_u32(sK + ((u - (int)ua) % KS) * C::kKVSlot);
+          const uint64_t b_k = make_sdesc(smem_u32(sK + ((u - (int)ua) % KS) * C::kKVSlot), 16, sbo, C::kSwz);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            if (elect_one())
-              mma_f16_ss_m(tmem + j * 256, make_sdesc(q0 + kk * 32, 16, sbo, C::kSwz),
-                           make_sdesc(k0 + kk * 32, 16, sbo, C::kSwz), idS, kk > 0, m0, m1, m2, m3);
+            for (int kk = 0; kk < D / 16; ++kk)
+              mma_f16_ss_m(tmem + s_col(b), desc_add(a_q, kk * 2), desc_add(b_k, kk * 2), idS, kk > 0,
+                           m0, m1, m2, m3);
+          }
           __syncwarp();
         }
         if (elect_one()) {
@@ -239,30 +281,35 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           mma_commit(&bars->q_empty[qs]);
         }
         __syncwarp();
-      };
-      issue_S(0);
+      }
+    }
+  } else if (warp == 10) {
+    // ===== PV issuer: O(b) = P(b) V as soon as the softmax of b has published P =====
+    if (nblk > 0) {
+      constexpr uint32_t idO = make_idesc_f16(kBF16, 128, D, false, true);
+      constexpr uint32_t sbo = 8 * C::kRowBytes;
       for (int b = 0; b < nblk; ++b) {
-        if (b + 1 < nblk) issue_S(b + 1);
-        const int j = b & 1;
+        const int j = b % NB;
         const int rs = r0 + b * kRows, re = min(rs + kRows, r1);
         const int u0 = rs / L, u1 = (re - 1) / L;
-        mbar_wait(&bars->p_ready[j], (b >> 1) & 1);
+        mbar_wait(&bars->p_ready[j], (b / NB) & 1);
         tc_fence_after();
         FTRACE(2, b);
+        const uint32_t tp = tmem + p_col(b), to = tmem + o_col(b);
         for (int u = u0; u <= u1; ++u) {
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
           const uint32_t m0 = lane_off(0, lo, hi), m1 = lane_off(1, lo, hi);
           const uint32_t m2 = lane_off(2, lo, hi), m3 = lane_off(3, lo, hi);
-          const uint32_t v0 = smem_u32(sV + ((u - (int)ua) % KS) * C::kKVSlot);
+          const uint64_t b_v = make_sdesc(smem_u32(sV + ((u - (int)ua) % KS) * C::kKVSlot), C::kKVSlot, sbo, C::kSwz);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < L / 16; ++kk)
-            if (elect_one())
-              mma_f16_ts_m(tmem + j * 256 + C::kOCol, tmem + j * 256 + kk * 8,
-                           make_sdesc(v0 + kk * 16 * C::kRowBytes, C::kKVSlot, sbo, C::kSwz), idO,
+            for (int kk = 0; kk < L / 16; ++kk)
+              mma_f16_ts_m(to, tp + kk * 8, desc_add(b_v, (kk * 16 * C::kRowBytes) >> 4), idO,
                            kk > 0, m0, m1, m2, m3);
+          }
           __syncwarp();
         }
-        // units whose last block is b: their K/V slots may be refilled
+        // units whose last block is b: their K/V slots may be refilled (S(b+1) does not use them)
         const int nxt_u0 = (b + 1 < nblk) ? (rs + kRows) / L : u1 + 1;
         if (elect_one()) {
           mma_commit(&bars->o_full[j]);
@@ -272,7 +319,7 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         __syncwarp();
       }
     }
-  } else {
+  } else if (warp < 10) {
     // ===== softmax + epilogue: group g takes blocks b = g, g+2, ... =====
     const int g = (warp - 2) >> 2;
     const int qd = warp & 3;
@@ -282,68 +329,59 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     uint8_t* stage = sO + g * C::kQBytes;
     const bool leader = (warp & 3) == 0 && lane == 0;   // one thread per group
     for (int b = g; b < nblk; b += 2) {
-      const int j = b & 1;
-      const uint32_t tb = tmem + t_lane + j * 256;
-      mbar_wait(&bars->s_full[j], (b >> 1) & 1);
+      const int j = b % NB;
+      const uint32_t tb = tmem + t_lane + s_col(b);
+      const uint32_t tpw = tmem + t_lane + p_col(b);
+      mbar_wait(&bars->s_full[j], (b / NB) & 1);
       tc_fence_after();
       if (leader) FTRACE(3, b);
       float mx = -INFINITY;
-#pragma unroll
-      for (int c0 = 0; c0 < L; c0 += 32) {           // pass 1: row max
-        uint32_t r[32];
-        if (c0 + 32 <= L) {
-          tmem_ld32(tb + c0, r);
-        } else {
-          tmem_ld16(tb + c0, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
-        }
-        tmem_wait_ld();
+      srow_stream<L>(tb, [&](int c0, const uint32_t* r) {   // pass 1: row max
 #pragma unroll
         for (int t = 0; t < 32; t += 2)
           if (c0 + t < L) mx = fmax3(mx, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
-      }
+      });
       const float mxs = mx * scale_log2;
       float sum0 = 0.f, sum1 = 0.f;
-#pragma unroll
-      for (int c0 = 0; c0 < L; c0 += 32) {           // pass 2: p = 2^(s*c - m*c), P over S
-        uint32_t r[32];
-        if (c0 + 32 <= L) {
-          tmem_ld32(tb + c0, r);
-        } else {
-          tmem_ld16(tb + c0, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
-        }
-        tmem_wait_ld();
+      if (C::kSplit && b >= 2) mbar_wait(&bars->buf_free[b & 1], ((b >> 1) - 1) & 1);   // P/O slot
+      srow_stream<L>(tb, [&](int c0, const uint32_t* r) {   // pass 2: p = 2^(s*c - m*c) -> P
         uint32_t pk[16];
 #pragma unroll
         for (int t = 0; t < 32; t += 2) {
           if (c0 + t < L) {
-            const float p0 = ex2(fmaf(__uint_as_float(r[t]), scale_log2, -mxs));
-            const float p1 = ex2(fmaf(__uint_as_float(r[t + 1]), scale_log2, -mxs));
+            // a quarter of the exponentials on the FMA pipe (columns 24..31 of each chunk)
+            const float a0 = fmaf(__uint_as_float(r[t]), scale_log2, -mxs);
+            const float a1 = fmaf(__uint_as_float(r[t + 1]), scale_log2, -mxs);
+            const float p0 = t >= 24 ? ex2_poly(a0) : ex2(a0);
+            const float p1 = t >= 24 ? ex2_poly(a1) : ex2(a1);
             sum0 += p0;
             sum1 += p1;
             pk[t >> 1] = fpack2<T>(p0, p1);
           }
         }
         if (c0 + 32 <= L) {
-          tmem_st16(tb + c0 / 2, pk);
+          tmem_st16(tpw + c0 / 2, pk);
         } else {
-          tmem_st8(tb + c0 / 2, pk);
+          tmem_st8(tpw + c0 / 2, pk);
         }
-      }
+      });
       tmem_wait_st();
       if (leader) FTRACE(4, b);
       const float inv = __frcp_rn(sum0 + sum1);
+      if (C::kSplit) sInv[(b & 1) * 128 + r_in] = inv;
       tc_fence_before();
       mbar_arrive(&bars->p_ready[j]);
+      if (C::kSplit) continue;   // the epilogue warpgroup drains O
 
       // ---- epilogue of block b ----
       const int rs = r0 + b * kRows, nrows = min(kRows, r1 - rs);
-      mbar_wait(&bars->o_full[j], (b >> 1) & 1);
+      mbar_wait(&bars->o_full[j], (b / NB) & 1);
       tc_fence_after();
       if (leader) FTRACE(5, b);
       uint32_t o[D];
 #pragma unroll
       for (int q = 0; q < D / 16; ++q)
-        tmem_ld16(tb + C::kOCol + q * 16, *reinterpret_cast<uint32_t(*)[16]>(&o[q * 16]));
+        tmem_ld16(tmem + t_lane + o_col(b) + q * 16, *reinterpret_cast<uint32_t(*)[16]>(&o[q * 16]));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bars->buf_free[j]);
@@ -359,6 +397,52 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             fpack2<T>(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
       fence_proxy_async_smem();
       named_sync(3 + g, 128);
+      if (leader) {
+        if (nrows == kRows) {
+          tma_store_3d(&tm_o, stage, 0, rs, 0);
+        } else {
+          for (int t = 0; t < nrows; t += 16)
+            tma_store_3d(&tm_o16, stage + t * C::kRowBytes, 0, rs + t, 0);
+        }
+        bulk_commit();
+      }
+      if (leader) FTRACE(6, b);
+    }
+    if (leader) bulk_wait_read<0>();
+  } else if (C::kSplit && warp >= 11) {
+    // ===== split mode: epilogue warpgroup (warps 11..14 = lane quarters 3, 0, 1, 2) =====
+    const int qd = warp & 3;
+    const int r_in = qd * 32 + lane;
+    const uint32_t t_lane = (uint32_t)(qd * 32) << 16;
+    const uint32_t oswz = (uint32_t)((r_in * C::kRowBytes) >> 7) & (C::kChunks - 1);
+    const bool leader = warp == 12 && lane == 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int rs = r0 + b * kRows, nrows = min(kRows, r1 - rs);
+      mbar_wait(&bars->o_full[b & 1], (b >> 1) & 1);
+      mbar_wait(&bars->p_ready[b & 1], (b >> 1) & 1);   // orders the softmax's sInv store
+      tc_fence_after();
+      if (leader) FTRACE(5, b);
+      uint32_t o[D];
+#pragma unroll
+      for (int q = 0; q < D / 16; ++q)
+        tmem_ld16(tmem + t_lane + o_col(b) + q * 16, *reinterpret_cast<uint32_t(*)[16]>(&o[q * 16]));
+      tmem_wait_ld();
+      const float inv = sInv[(b & 1) * 128 + r_in];
+      tc_fence_before();
+      mbar_arrive(&bars->buf_free[b & 1]);   // P/O slot reusable
+      uint8_t* stage = sO + (b & 1) * C::kQBytes;
+      if (leader) bulk_wait_read<1>();       // the store that last used this staging buffer
+      named_sync(1, 128);
+      uint8_t* orow = stage + r_in * C::kRowBytes;
+#pragma unroll
+      for (int c = 0; c < C::kChunks; ++c)
+        *reinterpret_cast<uint4*>(orow + ((c ^ oswz) << 4)) = make_uint4(
+            fpack2<T>(__uint_as_float(o[8 * c]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
+            fpack2<T>(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
+            fpack2<T>(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
+            fpack2<T>(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
+      fence_proxy_async_smem();
+      named_sync(2, 128);
       if (leader) {
         if (nrows == kRows) {
           tma_store_3d(&tm_o, stage, 0, rs, 0);
@@ -403,7 +487,7 @@ int launch_flat_t(const Geom& g, int dtype, const void* q, const void* k, const 
     }
     // every CTA gets >= 1 unit (ranges are balanced to within one unit)
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
-    rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kFThreads), (size_t)C::kSmem, s, m[0], m[1],
+    rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(C::kThreads), (size_t)C::kSmem, s, m[0], m[1],
                                m[2], m[3], m[4], (int64_t)g.units, g.scale * 1.4426950408889634f),
                     "fwd_flat_kernel launch");
     if (rc) return rc;
