@@ -344,6 +344,22 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Two ex2_poly lanes with packed f32x2 FMA/ADD (FFMA2 / FADD2: one issue slot per pair).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 kM = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, kM);
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
+  float2 p = __ffma2_rn(make_float2(0.05508868396282196f, 0.05508868396282196f), f,
+                        make_float2(0.24260404706001282f, 0.24260404706001282f));
+  p = __ffma2_rn(p, f, make_float2(0.6932762265205383f, 0.6932762265205383f));
+  p = __ffma2_rn(p, f, make_float2(0.9999289512634277f, 0.9999289512634277f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -54,6 +54,9 @@ using namespace sm100;
 // warps: 0 producer, 1 S issuer, 2..9 softmax (+ epilogue unless split), 10 PV issuer,
 // 11..14 epilogue (split mode)
 constexpr int kRows = 128;
+#ifndef FWA_POLY_FROM
+#define FWA_POLY_FROM 24   // columns [FWA_POLY_FROM, 32) of each 32-column piece use ex2_poly
+#endif
 
 // units intersecting one 128-row block: block starts are multiples of gcd(128, L) inside
 // a unit, so at most ceil((L - g + 128) / L) units.
@@ -342,21 +345,20 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           if (c0 + t < L) mx = fmax3(mx, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
       });
       const float mxs = mx * scale_log2;
-      float sum0 = 0.f, sum1 = 0.f;
+      float2 sum2 = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mxs, -mxs);
       if (C::kSplit && b >= 2) mbar_wait(&bars->buf_free[b & 1], ((b >> 1) - 1) & 1);   // P/O slot
       srow_stream<L>(tb, [&](int c0, const uint32_t* r) {   // pass 2: p = 2^(s*c - m*c) -> P
         uint32_t pk[16];
 #pragma unroll
         for (int t = 0; t < 32; t += 2) {
           if (c0 + t < L) {
-            // a quarter of the exponentials on the FMA pipe (columns 24..31 of each chunk)
-            const float a0 = fmaf(__uint_as_float(r[t]), scale_log2, -mxs);
-            const float a1 = fmaf(__uint_as_float(r[t + 1]), scale_log2, -mxs);
-            const float p0 = t >= 24 ? ex2_poly(a0) : ex2(a0);
-            const float p1 = t >= 24 ? ex2_poly(a1) : ex2(a1);
-            sum0 += p0;
-            sum1 += p1;
-            pk[t >> 1] = fpack2<T>(p0, p1);
+            // pairs on packed f32x2 FMA; a quarter of the exponentials (columns 24..31 of
+            // each piece) on the FMA pipe instead of the MUFU
+            const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[t]), __uint_as_float(r[t + 1])), sc2, nm2);
+            const float2 p = t >= FWA_POLY_FROM ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
+            sum2 = __fadd2_rn(sum2, p);
+            pk[t >> 1] = fpack2<T>(p.x, p.y);
           }
         }
         if (c0 + 32 <= L) {
@@ -367,7 +369,7 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       });
       tmem_wait_st();
       if (leader) FTRACE(4, b);
-      const float inv = __frcp_rn(sum0 + sum1);
+      const float inv = __frcp_rn(sum2.x + sum2.y);
       if (C::kSplit) sInv[(b & 1) * 128 + r_in] = inv;
       tc_fence_before();
       mbar_arrive(&bars->p_ready[j]);

@@ -492,18 +492,19 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       named_sync(1, 256);
       mx = fmaxf(rmax[r], rmax[128 + r]);
       const float mxs = mx * sl2;
-      float s0 = 0.f, s1 = 0.f;
+      float2 s2 = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-mxs, -mxs);
       tmem_stream<H>(ts, [&](int c, const uint32_t* x) {   // S read 2: p = 2^(s c - m c)
 #pragma unroll
         for (int t = 0; t < 8; t += 2) {
-          const float a = ex2(fmaf(__uint_as_float(x[t]), sl2, -mxs));
-          const float e = ex2(fmaf(__uint_as_float(x[t + 1]), sl2, -mxs));
-          s0 += a;
-          s1 += e;
-          pk[c * 4 + (t >> 1)] = bpack2<T>(a, e);
+          const float2 a = __ffma2_rn(make_float2(__uint_as_float(x[t]), __uint_as_float(x[t + 1])), sc2, nm2);
+          // a quarter of the exponentials on the FMA pipe
+          const float2 p = t == 6 ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
+          s2 = __fadd2_rn(s2, p);
+          pk[c * 4 + (t >> 1)] = bpack2<T>(p.x, p.y);
         }
       });
-      rsum[hf * 128 + r] = s0 + s1;
+      rsum[hf * 128 + r] = s2.x + s2.y;
       // p -> sP once the gradient MMAs of b-1 stopped reading it
       if (b > 0) mbar_wait(&bars->p_free, (b - 1) & 1);
 #pragma unroll
@@ -535,25 +536,24 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       fence_proxy_async_smem();
       mbar_arrive(&bars->p_ready);
       if (trc) BTRACE(5, b);
-      float rho0 = 0.f, rho1 = 0.f;
+      float2 rho2 = make_float2(0.f, 0.f);
       tmem_stream<H>(tdp, [&](int c, const uint32_t* x) {   // dP read 1: sum_j p dP
 #pragma unroll
-        for (int t = 0; t < 8; t += 2) {
-          const float2 p = bunpack2<T>(pk[c * 4 + (t >> 1)]);
-          rho0 = fmaf(p.x, __uint_as_float(x[t]), rho0);
-          rho1 = fmaf(p.y, __uint_as_float(x[t + 1]), rho1);
-        }
+        for (int t = 0; t < 8; t += 2)
+          rho2 = __ffma2_rn(bunpack2<T>(pk[c * 4 + (t >> 1)]),
+                            make_float2(__uint_as_float(x[t]), __uint_as_float(x[t + 1])), rho2);
       });
-      rrho[hf * 128 + r] = rho0 + rho1;
+      rrho[hf * 128 + r] = rho2.x + rho2.y;
       named_sync(1, 256);
       const float g = scale * inv_l;
       const float rg = (rrho[r] + rrho[128 + r]) * inv_l * g;   // rho * scale / l
+      const float2 g2 = make_float2(g, g), nrg2 = make_float2(-rg, -rg);
       tmem_stream<H>(tdp, [&](int c, const uint32_t* x) {   // dP read 2: dS
 #pragma unroll
         for (int t = 0; t < 8; t += 2) {
-          const float2 p = bunpack2<T>(pk[c * 4 + (t >> 1)]);
-          pk[c * 4 + (t >> 1)] = bpack2<T>(p.x * fmaf(__uint_as_float(x[t]), g, -rg),
-                                           p.y * fmaf(__uint_as_float(x[t + 1]), g, -rg));
+          const float2 d = __ffma2_rn(make_float2(__uint_as_float(x[t]), __uint_as_float(x[t + 1])), g2, nrg2);
+          const float2 v = __fmul2_rn(bunpack2<T>(pk[c * 4 + (t >> 1)]), d);
+          pk[c * 4 + (t >> 1)] = bpack2<T>(v.x, v.y);
         }
       });
       tc_fence_before();   // S / dP reads done before ds_ready lets S(b+1) overwrite them
