@@ -334,7 +334,7 @@ __host__ __device__ constexpr uint32_t make_idesc_f16(bool bf16, int M, int N, b
 // rounding), exponent added as an integer. Used for a share of the softmax exponentials
 // so the MUFU (16 ex2/clk/SM) is not the softmax bottleneck.
 __device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
+  x = fmaxf(x, -125.f);   // keeps the result exponent >= 1 (no wrap into the sign bit)
   const float t = x + 12582912.f;          // 1.5 * 2^23: round-to-nearest integer in the low bits
   const float j = t - 12582912.f;
   const float f = x - j;
@@ -346,8 +346,8 @@ __device__ __forceinline__ float ex2_poly(float x) {
 
 // Two ex2_poly lanes with packed f32x2 FMA/ADD (FFMA2 / FADD2: one issue slot per pair).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
+  x.x = fmaxf(x.x, -125.f);   // keeps the result exponent >= 1
+  x.y = fmaxf(x.y, -125.f);
   const float2 kM = make_float2(12582912.f, 12582912.f);
   const float2 t = __fadd2_rn(x, kM);
   const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));

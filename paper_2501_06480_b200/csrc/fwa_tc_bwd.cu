@@ -313,38 +313,55 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (j < L) mx = fmaxf(mx, __uint_as_float(s[j]));
+        for (int j = 0; j < 64; j += 2) {
+          if (j + 1 < L) {
+            float m3;
+            asm("max.f32 %0, %1, %2, %3;" : "=f"(m3) : "f"(mx), "f"(__uint_as_float(s[j])), "f"(__uint_as_float(s[j + 1])));
+            mx = m3;
+          } else if (j < L) {
+            mx = fmaxf(mx, __uint_as_float(s[j]));
+          }
+        }
       }
       const float mxs = ADD ? mx : mx * scale_log2;
       const float sl2 = ADD ? 1.f : scale_log2;
-      float sum = 0.f;
+      float2 sum2 = make_float2(0.f, 0.f);
+      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-mxs, -mxs);
 #pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const float p = j < L ? ex2(fmaf(__uint_as_float(s[j]), sl2, -mxs)) : 0.f;
-        s[j] = __float_as_uint(p);
-        sum += p;
+      for (int j = 0; j < 64; j += 2) {
+        // packed f32x2 math; a quarter of the exponentials on the FMA pipe (poly)
+        const float2 a = __ffma2_rn(make_float2(__uint_as_float(s[j]), __uint_as_float(s[j + 1])), sc2, nm2);
+        float2 p = (j & 7) == 6 ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
+        if (j >= L) p.x = 0.f;
+        if (j + 1 >= L) p.y = 0.f;
+        s[j] = __float_as_uint(p.x);
+        s[j + 1] = __float_as_uint(p.y);
+        sum2 = __fadd2_rn(sum2, p);
       }
-      const float inv = __frcp_rn(sum);
+      const float inv = __frcp_rn(sum2.x + sum2.y);
       // P (normalised) -> smem chunk by chunk; rho = sum_j P_j dP_j
       float rho = 0.f;
       uint8_t* prow = sP + prow_off;
+      float2 rho2 = make_float2(0.f, 0.f);
+      const float2 inv2 = make_float2(inv, inv);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint32_t w[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int j = 8 * c + 2 * t;
-          const float a = __uint_as_float(s[j]) * inv, b = __uint_as_float(s[j + 1]) * inv;
-          s[j] = __float_as_uint(a);
-          s[j + 1] = __float_as_uint(b);
-          if (j < L) rho = fmaf(a, __uint_as_float(dp[j]), rho);
-          if (j + 1 < L) rho = fmaf(b, __uint_as_float(dp[j + 1]), rho);
-          w[t] = pack2<T>(a, b);
+          const float2 pa = __fmul2_rn(make_float2(__uint_as_float(s[j]), __uint_as_float(s[j + 1])), inv2);
+          s[j] = __float_as_uint(pa.x);
+          s[j + 1] = __float_as_uint(pa.y);
+          // keys >= L carry p = 0, so they add nothing to rho
+          rho2 = __ffma2_rn(pa, make_float2(j < L ? __uint_as_float(dp[j]) : 0.f,
+                                            j + 1 < L ? __uint_as_float(dp[j + 1]) : 0.f), rho2);
+          w[t] = pack2<T>(pa.x, pa.y);
         }
         if (c < p_chunks)
           *reinterpret_cast<uint4*>(prow + ((c ^ pswz) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
+      rho = rho2.x + rho2.y;
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->p_ready);
