@@ -80,19 +80,28 @@ struct BFCfg {
   static constexpr int kRowBytes = D * 2;
   static constexpr int kTile = kRows * kRowBytes;        // one 128-row Q or dO block
   static constexpr int kNKT = (L + 127) / 128;           // 128-key tiles (M of dK/dV)
-  static constexpr int kAtoms = (L + 63) / 64;           // 64-key SW128 atom columns
-  static constexpr int kPBytes = kAtoms * 16384;         // sP / sDS: [128 rows][64 keys] atoms
+  // P / dS tiles: [128 rows][L keys] in 32-byte-swizzle atoms of 16 keys x 8 rows, atom
+  // columns of 16 keys 4 KB apart (K-major for dQ, MN-major for dV/dK). 16-key atoms keep
+  // L = 144 at 36 KB per tile (64-key atoms: 48 KB), which makes room for two dS buffers.
+  static constexpr int kAtoms = (L + 15) / 16;
+  static constexpr int kPBytes = kAtoms * 4096;
+  // the MN-major dK/dV reads of key tile kt span atoms [8kt, 8kt+8): up to kOver bytes past
+  // the last tile (garbage keys feed only lanes >= L, never stored) -- must stay in smem
+  static constexpr int kOver = (kNKT * 8 - kAtoms) * 4096;
   static constexpr int kKVBytes = L * kRowBytes;
   static constexpr int kKVSlot = (kKVBytes + 1023) / 1024 * 1024;
-  static constexpr int kBase = 1024 + 2 * kPBytes + kTile + 4096;
+  // dS buffers: 1 (K/V and Q/dO prefetch depth measured to matter more) or 2
+  static constexpr int kDSB = 1;
+  static constexpr int kBase = 1024 + (1 + kDSB) * kPBytes + kTile + 4096;   // sP, sDS[kDSB], staging
   // units touched between the oldest block with pending gradients and the newest S
   static constexpr int kNeedKV = span_units(L, 2 * kRows);
-  // Q/dO stages: 3 when the K/V ring still holds kNeedKV + 1 units (K/V prefetch measured
-  // to matter more than a third Q/dO stage), else 2
-  static constexpr int kQS = (kBase + 3 * 2 * kTile + (kNeedKV + 1) * 2 * kKVSlot <= 227 * 1024) ? 3 : 2;
+  // Q/dO stages: 3 when the K/V ring still holds kNeedKV units (the Q/dO slot of block b+2
+  // frees only when the gradients of block b-1 have executed), else 2
+  static constexpr int kQS = (kBase + 3 * 2 * kTile + kNeedKV * 2 * kKVSlot <= 227 * 1024) ? 3 : 2;
   static constexpr int kFixed = kBase + kQS * 2 * kTile;
   static constexpr int kKVAvail = (227 * 1024 - kFixed) / (2 * kKVSlot);
   static constexpr int kKS = kKVAvail < 6 ? kKVAvail : 6;
+  static_assert(kDSB == 1 || kDSB == 2, "dS buffers");
   static constexpr int kSmem = kFixed + kKS * 2 * kKVSlot;
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
   static constexpr int kChunks = kRowBytes / 16;
@@ -102,16 +111,13 @@ struct BFCfg {
   static constexpr uint32_t kTS = 0, kTDP = L, kTDQ = 2 * L;
   static constexpr uint32_t kTDV = 2 * L + D, kTDK = 2 * L + D + kVSets * kNKT * D;
   static constexpr int kCols = 2 * L + D + (kVSets + 1) * kNKT * D;
-  // the MN-major dK/dV reads of key tile kt span atoms [2kt, 2kt+2): the last one may run
-  // past sP's kAtoms (into sDS) or past sDS (into the Q/dO ring) -- in bounds, garbage
-  // keys feed only lanes >= L, which are never stored.
   static constexpr bool kFits = (L % 16 == 0) && kCols <= 512 && kKS >= kNeedKV &&
-                                kSmem <= 227 * 1024 && 2 * kNKT - kAtoms <= 1;
+                                kSmem <= 227 * 1024 && kOver <= kQS * 2 * kTile;
 };
 
 struct BFBarriers {
   uint64_t qd_full[3], qd_empty[3], kv_full[6], kv_empty[6];
-  uint64_t s_full, dp_full, p_ready, ds_ready, p_free, ds_free;
+  uint64_t s_full, dp_full, p_ready, ds_ready, p_free, ds_free[2];
   uint64_t acc_full, acc_free, dq_full, dq_free;
   uint64_t probe;
   uint32_t tmem_base;
@@ -150,9 +156,10 @@ __device__ __forceinline__ uint32_t blane_off(int w, int lo, int hi) {
   return ~in;
 }
 
-// byte offset of (row r, 8-key chunk c of atom column a) in a [128][keys] SW128 K-major tile
-__device__ __forceinline__ int patom_off(int a, int r, int c) {
-  return a * 16384 + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
+// byte offset of (row r, 8-key chunk at key `key`) in a [128 rows][keys] tile of 32-byte
+// swizzle atoms (16 keys x 8 rows, 256 B; 16-byte half index XOR address bit 7)
+__device__ __forceinline__ int patom_off(int r, int key) {
+  return (key >> 4) * 4096 + (r >> 3) * 256 + (r & 7) * 32 + ((((key >> 3) & 1) ^ ((r >> 2) & 1)) << 4);
 }
 
 // TMEM load of N (multiple of 8) consecutive columns into v[0..N); the start column is
@@ -198,8 +205,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sP = smem;
-  uint8_t* sDS = sP + C::kPBytes;
-  uint8_t* sQD = sDS + C::kPBytes;                   // [QS][Q | dO] blocks
+  uint8_t* sDS = sP + C::kPBytes;                    // [kDSB] dS tiles
+  uint8_t* sQD = sDS + C::kDSB * C::kPBytes;         // [QS][Q | dO] blocks
   uint8_t* sK = sQD + QS * 2 * C::kTile;             // [KS] K slots
   uint8_t* sV = sK + KS * C::kKVSlot;                // [KS] V slots
   uint8_t* sSt = sV + KS * C::kKVSlot;               // dQ / dK / dV store staging
@@ -227,7 +234,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     mbar_init(&bars->p_ready, 256);
     mbar_init(&bars->ds_ready, 256);
     mbar_init(&bars->p_free, 1);
-    mbar_init(&bars->ds_free, 1);
+    mbar_init(&bars->ds_free[0], 1);
+    mbar_init(&bars->ds_free[1], 1);
     mbar_init(&bars->acc_full, 1);
     mbar_init(&bars->acc_free, 128);
     mbar_init(&bars->dq_full, 1);
@@ -341,12 +349,12 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
           const uint32_t m0 = blane_off(0, lo, hi), m1 = blane_off(1, lo, hi);
           const uint32_t m2 = blane_off(2, lo, hi), m3 = blane_off(3, lo, hi);
-          const uint64_t a_ds = make_sdesc(ds0, 16, 1024, 2);
+          const uint64_t a_ds = make_sdesc(ds0 + (c % C::kDSB) * C::kPBytes, 16, 256, 6);
           const uint64_t b_k = make_sdesc(smem_u32(sK + kslot(u) * C::kKVSlot), C::kKVSlot, sbo, C::kSwz);
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < L / 16; ++kk)
-              mma_f16_ss_m(tmem + C::kTDQ, desc_add(a_ds, ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4),
+              mma_f16_ss_m(tmem + C::kTDQ, desc_add(a_ds, (kk * 4096) >> 4),
                            desc_add(b_k, (kk * 16 * C::kRowBytes) >> 4), idQ, kk > 0, m0, m1, m2, m3);
           }
           __syncwarp();
@@ -359,11 +367,14 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const int rs = r0 + c * kRows, re = min(rs + kRows, r1);
         const int u0 = rs / L, u1 = (re - 1) / L;
         mbar_wait(&bars->p_ready, c & 1);
-        mbar_wait(&bars->ds_ready, c & 1);
+        // ds_ready(c) was already waited by issue_SdP(c+1); waiting again could alias with
+        // phase c+1 now that dS is double-buffered (softmax may run a block ahead)
+        if (c == nblk - 1) mbar_wait(&bars->ds_ready, c & 1);
         tc_fence_after();
         if (lane == 0) BTRACE(1, c);
         const uint32_t q0 = smem_u32(sQD + qs * 2 * C::kTile), do0 = q0 + C::kTile;
-        const uint64_t a_p = make_sdesc(p0, 16384, 1024, 2), a_ds = make_sdesc(ds0, 16384, 1024, 2);
+        const uint64_t a_p = make_sdesc(p0, 4096, 256, 6);
+        const uint64_t a_ds = make_sdesc(ds0 + (c % C::kDSB) * C::kPBytes, 4096, 256, 6);
         const uint64_t b_do = make_sdesc(do0, C::kTile, sbo, C::kSwz);
         const uint64_t b_q = make_sdesc(q0, C::kTile, sbo, C::kSwz);
         // dV_kt(+)= p^T dO' / dK_kt(+)= dS^T Q over the segment's 16-row query steps
@@ -374,7 +385,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 #pragma unroll
               for (int kk = 0; kk < kRows / 16; ++kk)
                 mma_f16_ss_p(kk >= k_lo && kk < k_hi, tmem + col + kt * D,
-                             desc_add(a_p, (kt * 2 * 16384 + kk * 2048) >> 4),
+                             desc_add(a_p, (kt * 8 * 4096 + kk * 512) >> 4),
                              desc_add(b_do, (kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
           }
           __syncwarp();
@@ -386,7 +397,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 #pragma unroll
               for (int kk = 0; kk < kRows / 16; ++kk)
                 mma_f16_ss_p(kk >= k_lo && kk < k_hi, tmem + C::kTDK + kt * D,
-                             desc_add(a_ds, (kt * 2 * 16384 + kk * 2048) >> 4),
+                             desc_add(a_ds, (kt * 8 * 4096 + kk * 512) >> 4),
                              desc_add(b_q, (kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
           }
           __syncwarp();
@@ -436,14 +447,14 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const int nxt_u0 = (c + 1 < nblk) ? (rs + kRows) / L : u1 + 1;
         if (elect_one()) {
           if constexpr (!C::kDV2) mma_commit(&bars->p_free);
-          mma_commit(&bars->ds_free);
+          mma_commit(&bars->ds_free[c % C::kDSB]);
           mma_commit(&bars->qd_empty[qs]);
           for (int u = u0; u <= u1 && u < nxt_u0; ++u) mma_commit(&bars->kv_empty[kslot(u)]);
         }
         __syncwarp();
         if (lane == 0) BTRACE(2, c);
 #ifdef FWA_TC_ONLY
-        mbar_wait(&bars->ds_free, c & 1);   // timing experiment: when did the TC finish grads(c)?
+        mbar_wait(&bars->ds_free[c % C::kDSB], (c / C::kDSB) & 1);   // timing experiment: when did the TC finish grads(c)?
         if (lane == 0) BTRACE(14, c);
 #endif
       };
@@ -479,7 +490,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       tc_fence_after();
       mbar_arrive(&bars->p_ready);
       tc_fence_before();
-      if (b > 0) mbar_wait(&bars->ds_free, (b - 1) & 1);
+      if (b >= C::kDSB) mbar_wait(&bars->ds_free[b % C::kDSB], ((b / C::kDSB) - 1) & 1);
       mbar_arrive(&bars->ds_ready);
       continue;
 #endif
@@ -510,7 +521,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 #pragma unroll
       for (int c8 = 0; c8 < H / 8; ++c8) {
         const int key = hf * H + c8 * 8;
-        *reinterpret_cast<uint4*>(sP + patom_off(key >> 6, r, (key & 63) >> 3)) =
+        *reinterpret_cast<uint4*>(sP + patom_off(r, key)) =
             make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
       }
       if (trc) BTRACE(4, b);
@@ -557,11 +568,12 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         }
       });
       tc_fence_before();   // S / dP reads done before ds_ready lets S(b+1) overwrite them
-      if (b > 0) mbar_wait(&bars->ds_free, (b - 1) & 1);
+      if (b >= C::kDSB) mbar_wait(&bars->ds_free[b % C::kDSB], ((b / C::kDSB) - 1) & 1);   // buffer read
+      uint8_t* sDSb = sDS + (b % C::kDSB) * C::kPBytes;
 #pragma unroll
       for (int c8 = 0; c8 < H / 8; ++c8) {
         const int key = hf * H + c8 * 8;
-        *reinterpret_cast<uint4*>(sDS + patom_off(key >> 6, r, (key & 63) >> 3)) =
+        *reinterpret_cast<uint4*>(sDSb + patom_off(r, key)) =
             make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
       }
       fence_proxy_async_smem();

@@ -74,14 +74,16 @@ __global__ void k(unsigned long long* out, int iters, int klo, const uint8_t* gs
   } else if (BULK && threadIdx.x == 32) {
     // bulk global->smem copies (16 KB each) into a scratch region, back to back
     uint32_t ph = 0;
-    uint64_t off = 0;
+    uint64_t off = (uint64_t)blockIdx.x * 65536;
     while (!done) {
-      mbar_arrive_expect_tx(&bbar, 16384);
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];"
-                   ::"r"(smem_u32(s + 180224)), "l"(gsrc + off), "r"(smem_u32(&bbar)) : "memory");
+      // BULK copies of 4 KB in flight (the flat kernels keep ~16-48 KB of TMA loads in flight)
+      mbar_arrive_expect_tx(&bbar, 4096 * BULK);
+      for (int c = 0; c < BULK; ++c)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 4096, [%2];"
+                     ::"r"(smem_u32(s + 180224 + (c % 4) * 4096)), "l"(gsrc + off + c * 4096), "r"(smem_u32(&bbar)) : "memory");
       mbar_wait(&bbar, ph);
       ph ^= 1;
-      off = (off + 16384) % (1ull << 30);
+      off = (off + 4096 * BULK) % (1ull << 30);
     }
   }
   tc_fence_before();
@@ -108,6 +110,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&g, (1ull << 30) + 65536);
   run<0>(d, "full", klo, g);
   run<0, 1>(d, "full", klo, g);
-  run<1, 1>(d, "dV/dK only", klo, g);
+  run<0, 4>(d, "full", klo, g);
+  run<0, 12>(d, "full", klo, g);
   return 0;
 }
