@@ -114,7 +114,8 @@ int pick_fwd(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask, int
   if (tc_ok && d->kernel != FWA_KERNEL_GENERIC) {
     *kernel = FWA_KERNEL_TC;
     *smem = tc_small ? tc_fwd_smem(g, d->dtype) : tc_fwd_large_smem(g);
-    *tmem = tc_small ? tc_fwd_tmem_cols(g) : 256;
+    *tmem = tc_small ? tc_fwd_tmem_cols(g)
+                     : (tc_fwd_flat_supported(g, d->dtype, has_bias, has_mask) ? 512 : 256);
     return FWA_OK;
   }
   *kernel = FWA_KERNEL_GENERIC;
