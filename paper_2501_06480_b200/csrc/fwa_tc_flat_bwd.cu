@@ -41,7 +41,7 @@ extern "C" int fwa_bflat_trace_copy(long long* host) {
   do {                                                                  \
     if (blockIdx.x == 0 && (b) < 64) g_bflat_trace[ev][b] = clock64();  \
   } while (0)
-#ifdef FWA_TC_ONLY
+#ifdef FWA_PROBE
 // serialize: wait until every MMA issued so far has executed, then stamp event ev
 #define BPROBE(ev, b)                                   \
   do {                                                  \
@@ -61,6 +61,14 @@ extern "C" int fwa_bflat_trace_copy(long long* host) {
 #define BPROBE(ev, b) \
   do {                \
   } while (0)
+#endif
+
+#ifdef FWA_NO_MMA_FENCE
+#define MMA_FENCE_AFTER() \
+  do {                    \
+  } while (0)
+#else
+#define MMA_FENCE_AFTER() tc_fence_after()
 #endif
 
 namespace fwa {
@@ -172,6 +180,35 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* v) {
 #pragma unroll
   for (int c = c0; c + 16 <= N; c += 16) tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v + c));
   if constexpr ((N - c0) % 16 == 8) tmem_ld8(taddr + (N - 8), v + (N - 8));
+}
+
+// NKT key tiles x N query steps of M=128, K=16 SS MMAs (A MN-major from a P/dS tile:
+// key tile kt 8 atoms = 32 KB apart, step 512 B; B = 16 query rows of dO'/Q); the first
+// MMA of each key tile accumulates iff acc_first.
+template <int NKT, int D, int RB, int N>
+__device__ __forceinline__ void mma_steps_n(uint32_t dcol, uint64_t a0, uint64_t b0, uint32_t id,
+                                            uint32_t acc_first) {
+#pragma unroll
+  for (int kt = 0; kt < NKT; ++kt)
+#pragma unroll
+    for (int st = 0; st < N; ++st)
+      mma_f16_ss(dcol + kt * D, desc_add(a0, (kt * 8 * 4096 + st * 512) >> 4),
+                 desc_add(b0, (st * 16 * RB) >> 4), id, st > 0 ? 1u : acc_first);
+}
+template <int NKT, int D, int RB>
+__device__ __forceinline__ void mma_steps(int n, uint32_t dcol, uint64_t a0, uint64_t b0, uint32_t id,
+                                          uint32_t acc_first) {
+  switch (n) {
+    case 1: mma_steps_n<NKT, D, RB, 1>(dcol, a0, b0, id, acc_first); break;
+    case 2: mma_steps_n<NKT, D, RB, 2>(dcol, a0, b0, id, acc_first); break;
+    case 3: mma_steps_n<NKT, D, RB, 3>(dcol, a0, b0, id, acc_first); break;
+    case 4: mma_steps_n<NKT, D, RB, 4>(dcol, a0, b0, id, acc_first); break;
+    case 5: mma_steps_n<NKT, D, RB, 5>(dcol, a0, b0, id, acc_first); break;
+    case 6: mma_steps_n<NKT, D, RB, 6>(dcol, a0, b0, id, acc_first); break;
+    case 7: mma_steps_n<NKT, D, RB, 7>(dcol, a0, b0, id, acc_first); break;
+    case 8: mma_steps_n<NKT, D, RB, 8>(dcol, a0, b0, id, acc_first); break;
+    default: break;
+  }
 }
 
 // Streams N (multiple of 8) columns in 8-column pieces, the next piece's tcgen05.ld in
@@ -303,7 +340,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           mbar_wait(&bars->kv_full[lu % KS], (lu / KS) & 1);
         }
         if (b > 0) mbar_wait(&bars->ds_ready, (b - 1) & 1);   // S / dP of b-1 consumed
-        tc_fence_after();
+        MMA_FENCE_AFTER();
         if (lane == 0) BTRACE(0, b);
         const uint32_t q0 = smem_u32(sQD + qs * 2 * C::kTile), do0 = q0 + C::kTile;
         for (int u = u0; u <= u1; ++u) {
@@ -322,6 +359,9 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         }
         if (elect_one()) mma_commit(&bars->s_full);
         __syncwarp();
+#ifdef FWA_TC_ONLY
+        if (lane == 0) BTRACE(4, b);
+#endif
         for (int u = u0; u <= u1; ++u) {
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
           const uint32_t m0 = blane_off(0, lo, hi), m1 = blane_off(1, lo, hi);
@@ -338,13 +378,16 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         }
         if (elect_one()) mma_commit(&bars->dp_full);
         __syncwarp();
+#ifdef FWA_TC_ONLY
+        if (lane == 0) BTRACE(5, b);
+#endif
         BPROBE(15, b);
       };
       auto issue_dQ = [&](int c) {
         const int rs = r0 + c * kRows, re = min(rs + kRows, r1);
         const int u0 = rs / L, u1 = (re - 1) / L;
         if (c > 0) mbar_wait(&bars->dq_free, (c - 1) & 1);   // dQ(c-1) pulled out of TMEM
-        tc_fence_after();
+        MMA_FENCE_AFTER();
         for (int u = u0; u <= u1; ++u) {
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
           const uint32_t m0 = blane_off(0, lo, hi), m1 = blane_off(1, lo, hi);
@@ -370,7 +413,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         // ds_ready(c) was already waited by issue_SdP(c+1); waiting again could alias with
         // phase c+1 now that dS is double-buffered (softmax may run a block ahead)
         if (c == nblk - 1) mbar_wait(&bars->ds_ready, c & 1);
-        tc_fence_after();
+        MMA_FENCE_AFTER();
         if (lane == 0) BTRACE(1, c);
         const uint32_t q0 = smem_u32(sQD + qs * 2 * C::kTile), do0 = q0 + C::kTile;
         const uint64_t a_p = make_sdesc(p0, 4096, 256, 6);
@@ -378,28 +421,20 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const uint64_t b_do = make_sdesc(do0, C::kTile, sbo, C::kSwz);
         const uint64_t b_q = make_sdesc(q0, C::kTile, sbo, C::kSwz);
         // dV_kt(+)= p^T dO' / dK_kt(+)= dS^T Q over the segment's 16-row query steps
+        // dV_kt(+)= p^T dO' / dK_kt(+)= dS^T Q over the segment's 16-row query steps
+        // [k_lo, k_hi): straight-line MMAs per step count (no per-MMA predicate or branch)
         auto mma_dv = [&](uint32_t col, int k_lo, int k_hi, int first) {
-          if (elect_one()) {
-#pragma unroll
-            for (int kt = 0; kt < NKT; ++kt)
-#pragma unroll
-              for (int kk = 0; kk < kRows / 16; ++kk)
-                mma_f16_ss_p(kk >= k_lo && kk < k_hi, tmem + col + kt * D,
-                             desc_add(a_p, (kt * 8 * 4096 + kk * 512) >> 4),
-                             desc_add(b_do, (kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
-          }
+          const uint64_t a0 = desc_add(a_p, (k_lo * 512) >> 4);
+          const uint64_t b0 = desc_add(b_do, (k_lo * 16 * C::kRowBytes) >> 4);
+          if (elect_one())
+            mma_steps<NKT, D, C::kRowBytes>(k_hi - k_lo, tmem + col, a0, b0, idMN, first == k_lo ? 0u : 1u);
           __syncwarp();
         };
         auto mma_dk = [&](int k_lo, int k_hi, int first) {
-          if (elect_one()) {
-#pragma unroll
-            for (int kt = 0; kt < NKT; ++kt)
-#pragma unroll
-              for (int kk = 0; kk < kRows / 16; ++kk)
-                mma_f16_ss_p(kk >= k_lo && kk < k_hi, tmem + C::kTDK + kt * D,
-                             desc_add(a_ds, (kt * 8 * 4096 + kk * 512) >> 4),
-                             desc_add(b_q, (kk * 16 * C::kRowBytes) >> 4), idMN, kk != first);
-          }
+          const uint64_t a0 = desc_add(a_ds, (k_lo * 512) >> 4);
+          const uint64_t b0 = desc_add(b_q, (k_lo * 16 * C::kRowBytes) >> 4);
+          if (elect_one())
+            mma_steps<NKT, D, C::kRowBytes>(k_hi - k_lo, tmem + C::kTDK, a0, b0, idMN, first == k_lo ? 0u : 1u);
           __syncwarp();
         };
         if constexpr (C::kDV2) {
@@ -422,7 +457,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           if (starts && n_done > 0) {   // dK (and single-set dV) of the previous unit drained?
             if (lane == 0 && u > u0) BTRACE(11, c);
             mbar_wait(&bars->acc_free, (n_done - 1) & 1);
-            tc_fence_after();
+            MMA_FENCE_AFTER();
             if (lane == 0 && u > u0) BTRACE(12, c);
           }
           const int k_lo = (g_lo - rs) / 16, k_hi = (g_hi - rs) / 16;   // 16-row query steps
@@ -622,6 +657,11 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         if ((u + 1) * L > re) continue;   // unit continues into the next block
         mbar_wait(&bars->acc_full, n_unit & 1);
         tc_fence_after();
+#ifdef FWA_NO_DRAIN
+        mbar_arrive(&bars->acc_free);
+        ++n_unit;
+        continue;
+#endif
 #pragma unroll
         for (int kt = 0; kt < NKT; ++kt) {
           uint32_t gv[D], gk[D];
@@ -644,6 +684,10 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       }
       mbar_wait(&bars->dq_full, b & 1);
       tc_fence_after();
+#ifdef FWA_NO_DRAIN
+      mbar_arrive(&bars->dq_free);
+      continue;
+#endif
       uint32_t gq[D];
 #pragma unroll
       for (int q = 0; q < D / 16; ++q)
