@@ -227,7 +227,7 @@ extern "C" int fwa_fwd(const fwa_desc* desc, const void* q, const void* k, const
   if (kern == FWA_KERNEL_TC) {
     if (tc_fwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr))
       return launch_fwd_tc(g, desc->dtype, q, k, v, bias, mask, o, s);
-    return launch_fwd_tc_large(g, desc->dtype, q, k, v, o, s);
+    return launch_fwd_tc_large(g, desc->dtype, q, k, v, bias, mask, o, s);
   }
   return launch_fwd_generic(g, desc->dtype, q, k, v, bias, mask, o, s);
 }

@@ -118,14 +118,14 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 bool tc_fwd_large_supported(const Geom& g, int dtype, bool has_bias, bool has_mask);
 size_t tc_fwd_large_smem(const Geom& g);
 int launch_fwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                        void* o, cudaStream_t s);
+                        const float* bias, const float* mask, void* o, cudaStream_t s);
 
 // flat-row forward for 64 < L <= 256, L % 16 == 0 (fwa_tc_flat.cu); taken by
 // launch_fwd_tc_large when supported (FWA_NO_FLAT=1 disables it)
 bool tc_fwd_flat_supported(const Geom& g, int dtype, bool has_bias, bool has_mask);
 size_t tc_fwd_flat_smem(const Geom& g);
 int launch_fwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                       void* o, cudaStream_t s);
+                       const float* bias, const float* mask, void* o, cudaStream_t s);
 
 // tcgen05 / TMA backward (fwa_tc_bwd.cu)
 bool tc_bwd_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias);

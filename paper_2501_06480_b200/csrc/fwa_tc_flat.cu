@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <numeric>
+#include <type_traits>
 
 #include "fwa_common.cuh"
 #include "fwa_sm100.cuh"
@@ -158,11 +159,53 @@ __device__ __forceinline__ void srow_stream(uint32_t taddr, F&& f) {
   }
 }
 
-template <typename T, int D, int L>
+// Swin bias / shifted-window mask (ADD): `add` = (bias[h] + mask[w]) * log2e as f16, laid
+// out [w][h][L][L] (w = window index mod the mask period, h = head; unit u = (n, h) with
+// n = u / heads, w = n % n_w). Each softmax thread reads its row's L values from L2.
+struct FlatAdd {
+  const __half* table;
+  int heads;
+  int n_w;
+};
+
+// srow_stream plus the matching 32 f16 of this row's add table: piece c+1's TMEM and L2
+// loads are both in flight while f(first column, scores, adds) runs on piece c.
+template <int N, typename F>
+__device__ __forceinline__ void srow_stream_add(uint32_t taddr, const __half* arow, F&& f) {
+  // 16-column pieces (N % 16 == 0): 2 x (16 scores + 2 x 16 B of adds) in flight
+  uint32_t buf[2][16];
+  uint4 ab[2][2];
+  constexpr int kPieces = N / 16;
+  // volatile loads: kept in program order (plain __ldg gets hoisted for the whole row,
+  // which spills at L >= 128)
+  auto ldv4 = [](const __half* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+  };
+  auto load = [&](int c, uint32_t (&r)[16], uint4 (&a)[2]) {
+    tmem_ld16(taddr + c * 16, r);
+    a[0] = ldv4(arow + c * 16);
+    a[1] = ldv4(arow + c * 16 + 8);
+  };
+  load(0, buf[0], ab[0]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int c = 0; c < kPieces; ++c) {
+    if (c + 1 < kPieces) load(c + 1, buf[(c + 1) & 1], ab[(c + 1) & 1]);
+    f(c * 16, buf[c & 1], ab[c & 1]);
+    tmem_wait_ld();
+  }
+}
+
+template <typename T, int D, int L, bool ADD>
 __global__ void __launch_bounds__(FCfg<D, L>::kThreads, 1)
 fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-                const __grid_constant__ CUtensorMap tm_o16, int64_t n_units, float scale_log2) {
+                const __grid_constant__ CUtensorMap tm_o16, int64_t n_units, float scale_log2,
+                FlatAdd add) {
   using C = FCfg<D, L>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   constexpr int QS = C::kQStages, KS = C::kKVStages, NB = C::kNB;
@@ -339,23 +382,55 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       tc_fence_after();
       if (leader) FTRACE(3, b);
       float mx = -INFINITY;
-      srow_stream<L>(tb, [&](int c0, const uint32_t* r) {   // pass 1: row max
+      // this row's (bias + mask) * log2e (f16, L2-resident table); rows past the range clamp
+      const __half* arow = nullptr;
+      if constexpr (ADD) {
+        // 32-bit index math (rows < 2^31 is a precondition of the flat kernels)
+        const int grow = min(r0 + b * kRows + r_in, r1 - 1);
+        const int u = grow / L, i = grow - (grow / L) * L;
+        const int hd = u % add.heads, nw = (u / add.heads) % add.n_w;
+        arow = add.table + ((int64_t)(nw * add.heads + hd) * L + i) * L;
+      }
+      // scores in the exp2 domain: s * scale * log2e (+ add)
+      const float2 sc2 = make_float2(scale_log2, scale_log2);
+      if constexpr (ADD) {
+        // pass 1 with the add row: x = s*scale*log2e + add is written back over S (TMEM) so
+        // pass 2 reads it without touching the table again
+        srow_stream_add<L>(tb, arow, [&](int c0, const uint32_t* r, const uint4* a4) {
+          uint32_t xs[16];
 #pragma unroll
-        for (int t = 0; t < 32; t += 2)
-          if (c0 + t < L) mx = fmax3(mx, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
-      });
-      const float mxs = mx * scale_log2;
+          for (int t = 0; t < 16; t += 2) {
+            const uint32_t* aw = reinterpret_cast<const uint32_t*>(&a4[t / 8]);
+            const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&aw[(t % 8) / 2]));
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[t]), __uint_as_float(r[t + 1])), sc2, a);
+            mx = fmax3(mx, x.x, x.y);
+            xs[t] = __float_as_uint(x.x);
+            xs[t + 1] = __float_as_uint(x.y);
+          }
+          tmem_st16(tb + c0, xs);
+        });
+        tmem_wait_st();
+      } else {
+        srow_stream<L>(tb, [&](int c0, const uint32_t* r) {   // pass 1: row max
+#pragma unroll
+          for (int t = 0; t < 32; t += 2)
+            if (c0 + t < L) mx = fmax3(mx, __uint_as_float(r[t]), __uint_as_float(r[t + 1]));
+        });
+      }
+      const float mxs = ADD ? mx : mx * scale_log2;
       float2 sum2 = make_float2(0.f, 0.f);
-      const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mxs, -mxs);
+      const float2 nm2 = make_float2(-mxs, -mxs);
       if (C::kSplit && b >= 2) mbar_wait(&bars->buf_free[b & 1], ((b >> 1) - 1) & 1);   // P/O slot
-      srow_stream<L>(tb, [&](int c0, const uint32_t* r) {   // pass 2: p = 2^(s*c - m*c) -> P
+      // pass 2: p = 2^(x - m) -> P (x = s*scale*log2e, or the biased x already in TMEM)
+      const float2 sx2 = ADD ? make_float2(1.f, 1.f) : sc2;
+      srow_stream<L>(tb, [&](int c0, const uint32_t* r) {
         uint32_t pk[16];
 #pragma unroll
         for (int t = 0; t < 32; t += 2) {
           if (c0 + t < L) {
             // pairs on packed f32x2 FMA; a quarter of the exponentials (columns 24..31 of
             // each piece) on the FMA pipe instead of the MUFU
-            const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[t]), __uint_as_float(r[t + 1])), sc2, nm2);
+            const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[t]), __uint_as_float(r[t + 1])), sx2, nm2);
             const float2 p = t >= FWA_POLY_FROM ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
             sum2 = __fadd2_rn(sum2, p);
             pk[t >> 1] = fpack2<T>(p.x, p.y);
@@ -464,9 +539,24 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// (bias[h] + mask[w]) * log2e -> f16 table [n_w][h][L][L] (either input may be null)
+__global__ void flat_add_table_kernel(const float* __restrict__ bias, const float* __restrict__ mask,
+                                      int heads, int n_w, int L, __half* __restrict__ out) {
+  const int64_t LL = (int64_t)L * L, n = (int64_t)n_w * heads * LL;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ij = e % LL;
+    const int64_t h = (e / LL) % heads, w = e / (LL * heads);
+    float a = 0.f;
+    if (bias) a += bias[h * LL + ij];
+    if (mask) a += mask[w * LL + ij];
+    out[e] = __float2half_rn(a * 1.4426950408889634f);
+  }
+}
+
 template <typename T, int D, int L>
-int launch_flat_t(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
-                  cudaStream_t s) {
+int launch_flat_t(const Geom& g, int dtype, const void* q, const void* k, const void* v,
+                  const float* bias, const float* mask, void* o, cudaStream_t s) {
   using C = FCfg<D, L>;
   if constexpr (!C::kFits) {
     return fail(FWA_ERR_CAPACITY, "flat forward: shape does not fit");
@@ -479,19 +569,48 @@ int launch_flat_t(const Geom& g, int dtype, const void* q, const void* k, const 
     if ((rc = get_units_map(&m[2], v, dtype, 1, rows, D, L, 1))) return rc;
     if ((rc = get_units_map(&m[3], o, dtype, 1, rows, D, kRows, 1))) return rc;
     if ((rc = get_units_map(&m[4], o, dtype, 1, rows, D, 16, 1))) return rc;
-    auto kern = fwd_flat_kernel<T, D, L>;
-    static bool attr_done = false;
-    if (!attr_done) {
+    const bool add = bias || mask;
+    FlatAdd fa{nullptr, g.heads, 1};
+    if (add) {
+      // stream-ordered scratch for the combined f16 table (freed after the kernel)
+      fa.n_w = mask ? g.mask_windows : 1;
+      const size_t bytes = (size_t)fa.n_w * g.heads * L * L * sizeof(__half);
+      void* tab = nullptr;
+      static bool pool_kept = false;   // keep the stream-ordered pool's memory across calls
+      if (!pool_kept) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          uint64_t keep = ~0ull;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool_kept = true;
+      }
+      if ((rc = check_cuda(cudaMallocAsync(&tab, bytes, s), "cudaMallocAsync(add table)"))) return rc;
+      fa.table = static_cast<const __half*>(tab);
+      const int64_t n = (int64_t)fa.n_w * g.heads * L * L;
+      flat_add_table_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, s>>>(
+          bias, mask, g.heads, fa.n_w, L, static_cast<__half*>(tab));
+      if ((rc = check_cuda(cudaGetLastError(), "flat_add_table_kernel launch"))) return rc;
+      count_launch();
+    }
+    auto kern = add ? fwd_flat_kernel<T, D, L, true> : fwd_flat_kernel<T, D, L, false>;
+    static bool attr_done[2] = {false, false};
+    if (!attr_done[add]) {
       rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem),
                       "cudaFuncSetAttribute(fwd_flat)");
       if (rc) return rc;
-      attr_done = true;
+      attr_done[add] = true;
     }
     // every CTA gets >= 1 unit (ranges are balanced to within one unit)
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
     rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(C::kThreads), (size_t)C::kSmem, s, m[0], m[1],
-                               m[2], m[3], m[4], (int64_t)g.units, g.scale * 1.4426950408889634f),
+                               m[2], m[3], m[4], (int64_t)g.units, g.scale * 1.4426950408889634f, fa),
                     "fwd_flat_kernel launch");
+    if (add) {
+      const int rc2 = check_cuda(cudaFreeAsync(const_cast<__half*>(fa.table), s), "cudaFreeAsync(add table)");
+      if (!rc) rc = rc2;
+    }
     if (rc) return rc;
     count_launch();
     return FWA_OK;
@@ -499,21 +618,21 @@ int launch_flat_t(const Geom& g, int dtype, const void* q, const void* k, const 
 }
 
 template <typename T, int D>
-int flat_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, void* o,
-           cudaStream_t s) {
+int flat_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, const float* bias,
+           const float* mask, void* o, cudaStream_t s) {
   switch (g.L) {
-    case 80: return launch_flat_t<T, D, 80>(g, dtype, q, k, v, o, s);
-    case 96: return launch_flat_t<T, D, 96>(g, dtype, q, k, v, o, s);
-    case 112: return launch_flat_t<T, D, 112>(g, dtype, q, k, v, o, s);
-    case 128: return launch_flat_t<T, D, 128>(g, dtype, q, k, v, o, s);
-    case 144: return launch_flat_t<T, D, 144>(g, dtype, q, k, v, o, s);
-    case 160: return launch_flat_t<T, D, 160>(g, dtype, q, k, v, o, s);
-    case 176: return launch_flat_t<T, D, 176>(g, dtype, q, k, v, o, s);
-    case 192: return launch_flat_t<T, D, 192>(g, dtype, q, k, v, o, s);
-    case 208: return launch_flat_t<T, D, 208>(g, dtype, q, k, v, o, s);
-    case 224: return launch_flat_t<T, D, 224>(g, dtype, q, k, v, o, s);
-    case 240: return launch_flat_t<T, D, 240>(g, dtype, q, k, v, o, s);
-    case 256: return launch_flat_t<T, D, 256>(g, dtype, q, k, v, o, s);
+    case 80: return launch_flat_t<T, D, 80>(g, dtype, q, k, v, bias, mask, o, s);
+    case 96: return launch_flat_t<T, D, 96>(g, dtype, q, k, v, bias, mask, o, s);
+    case 112: return launch_flat_t<T, D, 112>(g, dtype, q, k, v, bias, mask, o, s);
+    case 128: return launch_flat_t<T, D, 128>(g, dtype, q, k, v, bias, mask, o, s);
+    case 144: return launch_flat_t<T, D, 144>(g, dtype, q, k, v, bias, mask, o, s);
+    case 160: return launch_flat_t<T, D, 160>(g, dtype, q, k, v, bias, mask, o, s);
+    case 176: return launch_flat_t<T, D, 176>(g, dtype, q, k, v, bias, mask, o, s);
+    case 192: return launch_flat_t<T, D, 192>(g, dtype, q, k, v, bias, mask, o, s);
+    case 208: return launch_flat_t<T, D, 208>(g, dtype, q, k, v, bias, mask, o, s);
+    case 224: return launch_flat_t<T, D, 224>(g, dtype, q, k, v, bias, mask, o, s);
+    case 240: return launch_flat_t<T, D, 240>(g, dtype, q, k, v, bias, mask, o, s);
+    case 256: return launch_flat_t<T, D, 256>(g, dtype, q, k, v, bias, mask, o, s);
   }
   return fail(FWA_ERR_CAPACITY, "flat forward: unsupported L");
 }
@@ -567,7 +686,9 @@ bool flat_disabled() {
 }  // namespace
 
 bool tc_fwd_flat_supported(const Geom& g, int dtype, bool has_bias, bool has_mask) {
-  if (flat_disabled() || has_bias || has_mask) return false;
+  (void)has_bias;
+  (void)has_mask;   // Swin bias / shifted-window mask: the ADD variant
+  if (flat_disabled()) return false;
   if (dtype != FWA_F16 && dtype != FWA_BF16) return false;
   if (g.L <= 64 || g.L > 256 || g.L % 16 != 0) return false;
   if (g.units * (int64_t)g.L >= ((int64_t)1 << 31)) return false;
@@ -589,15 +710,15 @@ size_t tc_fwd_flat_smem(const Geom& g) {
 }
 
 int launch_fwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                       void* o, cudaStream_t s) {
+                       const float* bias, const float* mask, void* o, cudaStream_t s) {
   const bool bf = dtype == FWA_BF16;
   switch (g.d) {
-    case 16: return bf ? flat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, o, s)
-                       : flat_l<__half, 16>(g, dtype, q, k, v, o, s);
-    case 32: return bf ? flat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, o, s)
-                       : flat_l<__half, 32>(g, dtype, q, k, v, o, s);
-    case 64: return bf ? flat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, o, s)
-                       : flat_l<__half, 64>(g, dtype, q, k, v, o, s);
+    case 16: return bf ? flat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, bias, mask, o, s)
+                       : flat_l<__half, 16>(g, dtype, q, k, v, bias, mask, o, s);
+    case 32: return bf ? flat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, bias, mask, o, s)
+                       : flat_l<__half, 32>(g, dtype, q, k, v, bias, mask, o, s);
+    case 64: return bf ? flat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, bias, mask, o, s)
+                       : flat_l<__half, 64>(g, dtype, q, k, v, bias, mask, o, s);
   }
   return fail(FWA_ERR_CAPACITY, "flat forward: unsupported head_dim");
 }

@@ -597,6 +597,7 @@ int large_dispatch_l(const Geom& g, int dtype, const void* q, const void* k, con
 }  // namespace
 
 bool tc_fwd_large_supported(const Geom& g, int dtype, bool has_bias, bool has_mask) {
+  if (tc_fwd_flat_supported(g, dtype, has_bias, has_mask)) return true;
   if (has_bias || has_mask) return false;
   if (dtype != FWA_F16 && dtype != FWA_BF16) return false;
   if (g.L <= 64 || g.L > 256) return false;
@@ -614,9 +615,10 @@ size_t tc_fwd_large_smem(const Geom& g) {
 }
 
 int launch_fwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                        void* o, cudaStream_t s) {
-  if (tc_fwd_flat_supported(g, dtype, false, false))
-    return launch_fwd_tc_flat(g, dtype, q, k, v, o, s);
+                        const float* bias, const float* mask, void* o, cudaStream_t s) {
+  if (tc_fwd_flat_supported(g, dtype, bias != nullptr, mask != nullptr))
+    return launch_fwd_tc_flat(g, dtype, q, k, v, bias, mask, o, s);
+  if (bias || mask) return fail(FWA_ERR_CAPACITY, "tcgen05 large-window forward: bias/mask need L % 16 == 0");
   const bool bf = dtype == FWA_BF16;
   switch (g.d) {
     case 16: return bf ? large_dispatch_l<__nv_bfloat16, 16>(g, dtype, q, k, v, o, s)

@@ -75,3 +75,33 @@ def test_flat_backward_matches_fp32(dt, units, L, d):
         assert err <= 2e-2, err
         assert torch.isfinite(got).all()
     assert fwa._native.device_flags() == 0
+
+
+def _ref_add(q, k, v, scale, bias, mask, heads):
+    s = (q.float() @ k.float().transpose(-1, -2)) * scale
+    N = q.shape[0]
+    if bias is not None:
+        s = s + bias[None]
+    if mask is not None:
+        s = s + mask[torch.arange(N, device=q.device) % mask.shape[0]][:, None]
+    return torch.softmax(s, -1) @ v.float()
+
+
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("N,h,L,d,nw,with_bias", [
+    (64, 4, 144, 32, 64, True), (37, 4, 144, 32, 4, True), (19, 8, 144, 32, 1, True),
+    (64, 4, 144, 32, 16, False), (40, 2, 256, 32, 4, True), (33, 3, 80, 16, 3, True),
+    (16, 4, 144, 64, 4, True),
+])
+def test_flat_forward_bias_mask_matches_fp32(dt, N, h, L, d, nw, with_bias):
+    rng = fwa.Rng(N * 13 + L + nw)
+    q, k, v = (fwa.fill_uniform(rng, (N, h, L, d), dtype=dt) for _ in range(3))
+    bias = fwa.fill_uniform(rng, (h, L, L), -0.5, 0.5) if with_bias else None
+    mask = torch.where(fwa.fill_uniform(rng, (nw, L, L)) > 0.6, -100.0, 0.0).float().contiguous() \
+        if nw > 1 or not with_bias else None
+    scale = d ** -0.5
+    o = ops.attention_forward(q, k, v, scale, bias, mask)
+    ref = _ref_add(q, k, v, scale, bias, mask, h)
+    err = (o.float() - ref).abs().max().item()
+    assert err <= 2e-2, err
+    assert fwa._native.device_flags() == 0
