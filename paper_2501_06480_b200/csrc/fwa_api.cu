@@ -13,6 +13,8 @@
 #include <mutex>
 #include <string>
 
+#include <algorithm>
+
 #include "fwa_common.cuh"
 
 namespace fwa {
@@ -239,7 +241,8 @@ extern "C" size_t fwa_bwd_workspace_bytes(const fwa_desc* desc, int want_dbias) 
   g.mask_windows = desc->mask_windows > 0 ? desc->mask_windows : 1;
   const size_t generic = (size_t)bwd_generic_grid(g) * g.heads * g.L * g.L * sizeof(float);
   const size_t tc = tc_bwd_workspace_bytes(g, desc->mask_windows > 0, true);
-  return generic > tc ? generic : tc;
+  const size_t flat = tc_bwd_flat_workspace_bytes(g);
+  return std::max(generic, std::max(tc, flat));
 }
 
 extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const void* v,
@@ -263,7 +266,8 @@ extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const
     if (tc_bwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr, dbias != nullptr))
       return launch_bwd_tc(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
                            (float*)workspace, (cudaStream_t)stream);
-    return launch_bwd_tc_large(g, desc->dtype, q, k, v, dout, dq, dk, dv, (cudaStream_t)stream);
+    return launch_bwd_tc_large(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
+                               (float*)workspace, (cudaStream_t)stream);
   }
   return launch_bwd_generic(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
                             (float*)workspace, (cudaStream_t)stream);

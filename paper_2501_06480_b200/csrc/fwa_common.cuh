@@ -127,6 +127,11 @@ size_t tc_fwd_flat_smem(const Geom& g);
 int launch_fwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                        const float* bias, const float* mask, void* o, cudaStream_t s);
 
+// (bias[h] + mask[w]) * log2e as f16 [n_w][h][L][L] in stream-ordered scratch (free with
+// cudaFreeAsync on the same stream after the kernel that reads it)
+int flat_build_add_table(const Geom& g, const float* bias, const float* mask, int* n_w, __half** out,
+                         cudaStream_t s);
+
 // tcgen05 / TMA backward (fwa_tc_bwd.cu)
 bool tc_bwd_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias);
 size_t tc_bwd_smem(const Geom& g);
@@ -140,13 +145,16 @@ int launch_bwd_tc(const Geom& g, int dtype, const void* q, const void* k, const 
 bool tc_bwd_large_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias);
 size_t tc_bwd_large_smem(const Geom& g);
 int launch_bwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                        const void* dout, void* dq, void* dk, void* dv, cudaStream_t s);
+                        const void* dout, const float* bias, const float* mask, void* dq, void* dk,
+                        void* dv, float* dbias, float* ws, cudaStream_t s);
 
 // flat-row backward (fwa_tc_flat_bwd.cu); taken by launch_bwd_tc_large when supported
 bool tc_bwd_flat_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias);
 size_t tc_bwd_flat_smem(const Geom& g);
+size_t tc_bwd_flat_workspace_bytes(const Geom& g);
 int launch_bwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                       const void* dout, void* dq, void* dk, void* dv, cudaStream_t s);
+                       const void* dout, const float* bias, const float* mask, void* dq, void* dk,
+                       void* dv, float* dbias, float* ws, cudaStream_t s);
 
 int device_sm_count();
 int64_t device_l2_bytes();

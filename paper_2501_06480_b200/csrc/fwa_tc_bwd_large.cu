@@ -512,9 +512,12 @@ size_t tc_bwd_large_smem(const Geom& g) {
 }
 
 int launch_bwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                        const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
-  if (tc_bwd_flat_supported(g, dtype, false, false, false))
-    return launch_bwd_tc_flat(g, dtype, q, k, v, dout, dq, dk, dv, s);
+                        const void* dout, const float* bias, const float* mask, void* dq, void* dk,
+                        void* dv, float* dbias, float* ws, cudaStream_t s) {
+  if (tc_bwd_flat_supported(g, dtype, bias != nullptr, mask != nullptr, dbias != nullptr))
+    return launch_bwd_tc_flat(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
+  if (bias || mask || dbias)
+    return fail(FWA_ERR_CAPACITY, "tcgen05 large-window backward: bias/mask not supported here");
   const bool bf = dtype == FWA_BF16;
   switch (g.d) {
     case 16: return bf ? bwd_large_l<__nv_bfloat16, 16>(g, dtype, q, k, v, dout, dq, dk, dv, s)

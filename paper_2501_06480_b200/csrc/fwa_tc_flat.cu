@@ -572,27 +572,9 @@ int launch_flat_t(const Geom& g, int dtype, const void* q, const void* k, const 
     const bool add = bias || mask;
     FlatAdd fa{nullptr, g.heads, 1};
     if (add) {
-      // stream-ordered scratch for the combined f16 table (freed after the kernel)
-      fa.n_w = mask ? g.mask_windows : 1;
-      const size_t bytes = (size_t)fa.n_w * g.heads * L * L * sizeof(__half);
-      void* tab = nullptr;
-      static bool pool_kept = false;   // keep the stream-ordered pool's memory across calls
-      if (!pool_kept) {
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-          uint64_t keep = ~0ull;
-          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-        pool_kept = true;
-      }
-      if ((rc = check_cuda(cudaMallocAsync(&tab, bytes, s), "cudaMallocAsync(add table)"))) return rc;
-      fa.table = static_cast<const __half*>(tab);
-      const int64_t n = (int64_t)fa.n_w * g.heads * L * L;
-      flat_add_table_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, s>>>(
-          bias, mask, g.heads, fa.n_w, L, static_cast<__half*>(tab));
-      if ((rc = check_cuda(cudaGetLastError(), "flat_add_table_kernel launch"))) return rc;
-      count_launch();
+      __half* tab = nullptr;
+      if ((rc = flat_build_add_table(g, bias, mask, &fa.n_w, &tab, s))) return rc;
+      fa.table = tab;
     }
     auto kern = add ? fwd_flat_kernel<T, D, L, true> : fwd_flat_kernel<T, D, L, false>;
     static bool attr_done[2] = {false, false};
@@ -684,6 +666,32 @@ bool flat_disabled() {
 }
 
 }  // namespace
+
+int flat_build_add_table(const Geom& g, const float* bias, const float* mask, int* n_w, __half** out,
+                         cudaStream_t s) {
+  // stream-ordered scratch for the combined f16 table (the caller frees it after its kernel)
+  static bool pool_kept = false;   // keep the pool's memory across calls (no re-mapping)
+  if (!pool_kept) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_kept = true;
+  }
+  *n_w = mask ? g.mask_windows : 1;
+  const int64_t n = (int64_t)*n_w * g.heads * g.L * g.L;
+  void* tab = nullptr;
+  int rc = check_cuda(cudaMallocAsync(&tab, (size_t)n * sizeof(__half), s), "cudaMallocAsync(add table)");
+  if (rc) return rc;
+  flat_add_table_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, s>>>(
+      bias, mask, g.heads, *n_w, g.L, static_cast<__half*>(tab));
+  if ((rc = check_cuda(cudaGetLastError(), "flat_add_table_kernel launch"))) return rc;
+  count_launch();
+  *out = static_cast<__half*>(tab);
+  return FWA_OK;
+}
 
 bool tc_fwd_flat_supported(const Geom& g, int dtype, bool has_bias, bool has_mask) {
   (void)has_bias;

@@ -226,14 +226,24 @@ __device__ __forceinline__ void tmem_stream(uint32_t taddr, F&& f) {
   }
 }
 
-template <typename T, int D, int L>
+// Swin bias / shifted-window mask for the backward: the same f16 (bias + mask) * log2e
+// table as the forward; with dBias each CTA accumulates P (dP - rho) of its rows into its
+// own [heads][L][L] fp32 slice of `ws` (reduced over CTAs in a fixed order afterwards).
+struct FlatBAdd {
+  const __half* table;
+  int heads;
+  int n_w;
+  float* ws;
+};
+
+template <typename T, int D, int L, bool ADD, bool DBIAS>
 __global__ void __launch_bounds__(kBThreads, 1)
 bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                 const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dq16,
                 const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dk16,
                 const __grid_constant__ CUtensorMap tm_dv, const __grid_constant__ CUtensorMap tm_dv16,
-                int64_t n_units, float scale) {
+                int64_t n_units, float scale, FlatBAdd add) {
   using C = BFCfg<D, L>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   constexpr int QS = C::kQS, KS = C::kKS, NKT = C::kNKT;
@@ -287,6 +297,11 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     tma_prefetch_desc(&tm_do);
   }
   if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
+  if constexpr (DBIAS) {
+    griddep_wait();   // the slice may still be read by the previous call's reduction
+    float4* z = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.heads * L * L);
+    for (int i = threadIdx.x; i < add.heads * L * L / 4; i += kBThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -514,6 +529,18 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     uint32_t pk[H / 2];   // this half row of p (then dS) as 16-bit pairs
     for (int b = 0; b < nblk; ++b) {
       const int qs = b % QS;
+      // this row's (unit, query) -> (head, window); rows past the range clamp to the last one
+      const int grow = min(r0 + b * kRows + r, r1 - 1);
+      const int urow = grow / L, irow = grow - (grow / L) * L;
+      const int hrow = ADD ? urow % add.heads : 0;
+      uint4 arow_half[ADD ? H / 8 : 1];
+      if constexpr (ADD) {
+        const int wrow = (urow / add.heads) % add.n_w;
+        const uint4* ap = reinterpret_cast<const uint4*>(
+            add.table + ((int64_t)(wrow * add.heads + hrow) * L + irow) * L + hf * H);
+#pragma unroll
+        for (int c = 0; c < H / 8; ++c) arow_half[c] = __ldg(ap + c);
+      }
       mbar_wait(&bars->s_full, b & 1);
       tc_fence_after();
       const bool trc = warp == 4 && lane == 0;
@@ -530,16 +557,37 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       continue;
 #endif
       float mx = -INFINITY;
-      tmem_stream<H>(ts, [&](int c, const uint32_t* x) {   // S read 1: row max
+      if constexpr (ADD) {
+        // S read 1 with this half row of (bias + mask) * log2e: x = s*scale*log2e + add is
+        // written back over S so read 2 does not touch the table again
+        const float2 sc2a = make_float2(sl2, sl2);
+        tmem_stream<H>(ts, [&](int c, const uint32_t* x) {
+          const uint4 aw = arow_half[c];
+          const uint32_t a4[4] = {aw.x, aw.y, aw.z, aw.w};
+          uint32_t xs[8];
 #pragma unroll
-        for (int t = 0; t < 8; t += 2) mx = bfmax3(mx, __uint_as_float(x[t]), __uint_as_float(x[t + 1]));
-      });
+          for (int t = 0; t < 8; t += 2) {
+            const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&a4[t / 2]));
+            const float2 v = __ffma2_rn(make_float2(__uint_as_float(x[t]), __uint_as_float(x[t + 1])), sc2a, a);
+            mx = bfmax3(mx, v.x, v.y);
+            xs[t] = __float_as_uint(v.x);
+            xs[t + 1] = __float_as_uint(v.y);
+          }
+          tmem_st8(ts + c * 8, xs);
+        });
+        tmem_wait_st();
+      } else {
+        tmem_stream<H>(ts, [&](int c, const uint32_t* x) {   // S read 1: row max
+#pragma unroll
+          for (int t = 0; t < 8; t += 2) mx = bfmax3(mx, __uint_as_float(x[t]), __uint_as_float(x[t + 1]));
+        });
+      }
       rmax[hf * 128 + r] = mx;
       named_sync(1, 256);
       mx = fmaxf(rmax[r], rmax[128 + r]);
-      const float mxs = mx * sl2;
+      const float mxs = ADD ? mx : mx * sl2;
       float2 s2 = make_float2(0.f, 0.f);
-      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-mxs, -mxs);
+      const float2 sc2 = ADD ? make_float2(1.f, 1.f) : make_float2(sl2, sl2), nm2 = make_float2(-mxs, -mxs);
       tmem_stream<H>(ts, [&](int c, const uint32_t* x) {   // S read 2: p = 2^(s c - m c)
 #pragma unroll
         for (int t = 0; t < 8; t += 2) {
@@ -614,6 +662,40 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       fence_proxy_async_smem();
       mbar_arrive(&bars->ds_ready);
       if (trc) BTRACE(6, b);
+      if constexpr (DBIAS) {
+        // dBias partial: += dS / scale = P (dP - rho), rows of this CTA's range only
+        if (r0 + b * kRows + r < r1) {
+          float4* wp = reinterpret_cast<float4*>(add.ws + ((size_t)blockIdx.x * add.heads + hrow) * L * L +
+                                                 (size_t)irow * L + hf * H);
+          const float is = 1.f / scale;
+#pragma unroll
+          for (int c8 = 0; c8 < H / 8; c8 += 3) {
+            float4 acc[6];
+#pragma unroll
+            for (int e = 0; e < 3; ++e)
+              if (c8 + e < H / 8) {
+                acc[2 * e] = wp[2 * (c8 + e)];
+                acc[2 * e + 1] = wp[2 * (c8 + e) + 1];
+              }
+#pragma unroll
+            for (int e = 0; e < 3; ++e)
+              if (c8 + e < H / 8) {
+                float f[8];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  const float2 v = bunpack2<T>(pk[4 * (c8 + e) + t]);
+                  f[2 * t] = v.x * is;
+                  f[2 * t + 1] = v.y * is;
+                }
+                acc[2 * e] = make_float4(acc[2 * e].x + f[0], acc[2 * e].y + f[1], acc[2 * e].z + f[2], acc[2 * e].w + f[3]);
+                acc[2 * e + 1] = make_float4(acc[2 * e + 1].x + f[4], acc[2 * e + 1].y + f[5],
+                                             acc[2 * e + 1].z + f[6], acc[2 * e + 1].w + f[7]);
+                wp[2 * (c8 + e)] = acc[2 * e];
+                wp[2 * (c8 + e) + 1] = acc[2 * e + 1];
+              }
+          }
+        }
+      }
     }
   } else {
     // ===== drain warps: dK/dV of finished units, dQ of every block =====
@@ -706,9 +788,20 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// dbias[h][i][j] = sum over CTAs c (ascending) of ws[c][h][i][j]: fixed order, deterministic
+__global__ void bflat_dbias_reduce_kernel(const float* __restrict__ ws, int grid, int n,
+                                          float* __restrict__ dbias) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int c = 0; c < grid; ++c) acc += ws[(size_t)c * n + e];
+    dbias[e] = acc;
+  }
+}
+
 template <typename T, int D, int L>
 int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                   const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
+                   const void* dout, const float* bias, const float* mask, void* dq, void* dk,
+                   void* dv, float* dbias, float* ws, cudaStream_t s) {
   using C = BFCfg<D, L>;
   if constexpr (!C::kFits) {
     return fail(FWA_ERR_CAPACITY, "flat backward: shape does not fit");
@@ -725,21 +818,53 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
       if ((rc = get_units_map(&m[4 + 2 * i], outs[i], dtype, 1, rows, D, kRows, 1))) return rc;
       if ((rc = get_units_map(&m[5 + 2 * i], outs[i], dtype, 1, rows, D, 16, 1))) return rc;
     }
-    auto kern = bwd_flat_kernel<T, D, L>;
-    static bool attr_done = false;
-    if (!attr_done) {
+    const bool add = bias || mask;
+    const bool want_db = dbias != nullptr;
+    FlatBAdd fa{nullptr, g.heads, 1, ws};
+    if (add) {
+      if constexpr (D != 32) {
+        return fail(FWA_ERR_CAPACITY, "flat backward: bias/mask need d = 32");
+      } else {
+        __half* tab = nullptr;
+        if ((rc = flat_build_add_table(g, bias, mask, &fa.n_w, &tab, s))) return rc;
+        fa.table = tab;
+      }
+    }
+    // kernel variants: plain, + bias/mask, + bias/mask + dBias (bias/mask only for d = 32)
+    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
+                 CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, int64_t, float, FlatBAdd) =
+        bwd_flat_kernel<T, D, L, false, false>;
+    int variant = 0;
+    if constexpr (D == 32) {
+      if (add) {
+        kern = want_db ? bwd_flat_kernel<T, D, L, true, true> : bwd_flat_kernel<T, D, L, true, false>;
+        variant = want_db ? 2 : 1;
+      }
+    }
+    static bool attr_done[3] = {false, false, false};
+    if (!attr_done[variant]) {
       rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem),
                       "cudaFuncSetAttribute(bwd_flat)");
       if (rc) return rc;
-      attr_done = true;
+      attr_done[variant] = true;
     }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
     rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kBThreads), (size_t)C::kSmem, s, m[0], m[1],
                                m[2], m[3], m[4], m[5], m[6], m[7], m[8], m[9], (int64_t)g.units,
-                               g.scale),
+                               g.scale, fa),
                     "bwd_flat_kernel launch");
+    if (!rc) count_launch();
+    if (add) {
+      const int rc2 = check_cuda(cudaFreeAsync(const_cast<__half*>(fa.table), s), "cudaFreeAsync(add table)");
+      if (!rc) rc = rc2;
+    }
     if (rc) return rc;
-    count_launch();
+    if (want_db) {
+      const int n = g.heads * L * L;
+      bflat_dbias_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(ws, grid, n, dbias);
+      if ((rc = check_cuda(cudaGetLastError(), "bflat_dbias_reduce_kernel launch"))) return rc;
+      count_launch();
+    }
     return FWA_OK;
   }
 }
@@ -748,10 +873,11 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
 
 template <typename T, int D>
 int bflat_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, const void* dout,
-            void* dq, void* dk, void* dv, cudaStream_t s) {
+            const float* bias, const float* mask, void* dq, void* dk, void* dv, float* dbias,
+            float* ws, cudaStream_t s) {
   switch (g.L) {
 #define FWA_CASE(LL) \
-  case LL: return launch_bflat_t<T, D, LL>(g, dtype, q, k, v, dout, dq, dk, dv, s);
+  case LL: return launch_bflat_t<T, D, LL>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
     FWA_FLAT_LS(FWA_CASE)
 #undef FWA_CASE
   }
@@ -791,7 +917,12 @@ bool bflat_disabled() {
 }  // namespace
 
 bool tc_bwd_flat_supported(const Geom& g, int dtype, bool has_bias, bool has_mask, bool want_dbias) {
-  if (bflat_disabled() || has_bias || has_mask || want_dbias) return false;
+  if (bflat_disabled()) return false;
+  if (want_dbias && !has_bias) return false;
+  // bias/mask variants are built for d = 32 (Swin); with dBias, the rows of one 128-row block
+  // must hit distinct [head][query] slices of the per-CTA partials (no two threads on one row)
+  if ((has_bias || has_mask) && g.d != 32) return false;
+  if (want_dbias && g.heads < 2 && g.L < 128) return false;
   if (dtype != FWA_F16 && dtype != FWA_BF16) return false;
   if (g.L <= 64 || g.L > 256 || g.L % 16 != 0) return false;
   if (g.units * (int64_t)g.L >= ((int64_t)1 << 31)) return false;
@@ -812,16 +943,22 @@ size_t tc_bwd_flat_smem(const Geom& g) {
   return 0;
 }
 
+size_t tc_bwd_flat_workspace_bytes(const Geom& g) {
+  return (size_t)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count())) * g.heads * g.L *
+         g.L * sizeof(float);
+}
+
 int launch_bwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                       const void* dout, void* dq, void* dk, void* dv, cudaStream_t s) {
+                       const void* dout, const float* bias, const float* mask, void* dq, void* dk,
+                       void* dv, float* dbias, float* ws, cudaStream_t s) {
   const bool bf = dtype == FWA_BF16;
   switch (g.d) {
-    case 16: return bf ? bflat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, dout, dq, dk, dv, s)
-                       : bflat_l<__half, 16>(g, dtype, q, k, v, dout, dq, dk, dv, s);
-    case 32: return bf ? bflat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, dout, dq, dk, dv, s)
-                       : bflat_l<__half, 32>(g, dtype, q, k, v, dout, dq, dk, dv, s);
-    case 64: return bf ? bflat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, dout, dq, dk, dv, s)
-                       : bflat_l<__half, 64>(g, dtype, q, k, v, dout, dq, dk, dv, s);
+    case 16: return bf ? bflat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s)
+                       : bflat_l<__half, 16>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
+    case 32: return bf ? bflat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s)
+                       : bflat_l<__half, 32>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
+    case 64: return bf ? bflat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s)
+                       : bflat_l<__half, 64>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
   }
   return fail(FWA_ERR_CAPACITY, "flat backward: unsupported head_dim");
 }

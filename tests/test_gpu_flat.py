@@ -105,3 +105,50 @@ def test_flat_forward_bias_mask_matches_fp32(dt, N, h, L, d, nw, with_bias):
     err = (o.float() - ref).abs().max().item()
     assert err <= 2e-2, err
     assert fwa._native.device_flags() == 0
+
+
+def _ref_add_bwd(q, k, v, do, scale, bias, mask):
+    qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
+    bf = bias.float().clone().requires_grad_(True) if bias is not None else None
+    s = (qf @ kf.transpose(-1, -2)) * scale
+    N = q.shape[0]
+    if bf is not None:
+        s = s + bf[None]
+    if mask is not None:
+        s = s + mask[torch.arange(N, device=q.device) % mask.shape[0]][:, None]
+    (torch.softmax(s, -1) @ vf).backward(do.float())
+    return qf.grad, kf.grad, vf.grad, (bf.grad if bf is not None else None)
+
+
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("N,h,L,nw,with_bias,want_db", [
+    (64, 4, 144, 64, True, True), (37, 4, 144, 4, True, True), (19, 8, 144, 1, True, True),
+    (64, 4, 144, 16, False, False), (33, 4, 144, 4, True, False), (24, 2, 96, 4, True, True),
+    (10, 3, 256, 4, True, True), (9, 1, 144, 3, True, True),
+])
+def test_flat_backward_bias_mask_dbias_matches_fp32(dt, N, h, L, nw, with_bias, want_db):
+    d = 32
+    rng = fwa.Rng(N * 29 + L + nw)
+    q, k, v, do = (fwa.fill_uniform(rng, (N, h, L, d), dtype=dt) for _ in range(4))
+    bias = fwa.fill_uniform(rng, (h, L, L), -0.5, 0.5) if with_bias else None
+    mask = torch.where(fwa.fill_uniform(rng, (nw, L, L)) > 0.6, -100.0, 0.0).float().contiguous() \
+        if nw > 1 or not with_bias else None
+    scale = d ** -0.5
+    fp = ops.footprint(N, h, L, d, dt)
+    assert fp["kernel_bwd"] == "tc"
+    dq, dk, dv, db = ops.attention_backward(q, k, v, do, scale, bias, mask, want_dbias=want_db)
+    rq, rk, rv, rb = _ref_add_bwd(q, k, v, do, scale, bias, mask)
+    for got, want in zip((dq, dk, dv), (rq, rk, rv)):
+        assert (got.float() - want).abs().max().item() <= 2e-2
+    if want_db:
+        tol = 2e-2 * max(1.0, rb.abs().max().item())
+        assert (db - rb).abs().max().item() <= tol
+    assert fwa._native.device_flags() == 0
+
+
+def test_flat_backward_dbias_is_deterministic():
+    rng = fwa.Rng(3)
+    q, k, v, do = (fwa.fill_uniform(rng, (40, 4, 144, 32), dtype=torch.float16) for _ in range(4))
+    bias = fwa.fill_uniform(rng, (4, 144, 144), -0.5, 0.5)
+    outs = [ops.attention_backward(q, k, v, do, 0.2, bias, None, want_dbias=True)[3] for _ in range(3)]
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
