@@ -14,7 +14,7 @@ relative-position bias on every layer (learnable: dBias computed), shifted-windo
 mask on the SW-MSA layers, forward + backward) measured the same way.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fwa|reference]
-                  [--workload swin_t_fwd|swin_t_fwdbwd|swin_b_fwdbwd|large_sweep]
+                  [--workload swin_t_fwd|swin_t_fwdbwd|swin_b_fwdbwd|swin_b_train|large_sweep]
 
 Multi-GPU: torchrun, one process per GPU, weak scaling (B images per rank), no
 collective on the hot path; barrier + synchronize around the timed region,
@@ -50,6 +50,10 @@ WORKLOADS = {
     "swin_b_fwdbwd": dict(layers=SWIN_B384, batch=64, dtype="float16", bwd=True, extras=False,
                           k=12, desc="Swin-B 384^2 window 12 B=64, fp16 forward+backward "
                                      "(configs[3])"),
+    "swin_b_train": dict(layers=SWIN_B384, batch=64, dtype="bfloat16", bwd=True, extras=True,
+                         k=12, desc="Swin-B 384^2 window 12 B=64, rel-pos bias (learnable) + "
+                                    "shifted-window mask on SW-MSA layers, bf16 forward+backward "
+                                    "(configs[3] with configs[2]'s training extras)"),
     "large_sweep": dict(layers=LARGE, batch=1, cpu_div=512, dtype="float16", bwd=False, extras=False, k=8,
                         desc="large-window sweep L=64/256, d=32/64, ~1 GB per call, fp16 "
                              "forward (configs[4])"),
