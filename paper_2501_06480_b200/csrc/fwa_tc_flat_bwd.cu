@@ -668,31 +668,21 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           float4* wp = reinterpret_cast<float4*>(add.ws + ((size_t)blockIdx.x * add.heads + hrow) * L * L +
                                                  (size_t)irow * L + hf * H);
           const float is = 1.f / scale;
+          // fire-and-forget vector reductions (no load round trip). One thread owns a
+          // [head][query] row of this CTA's slice per block and consecutive blocks are
+          // separated by the softmax warpgroup's barriers, so the per-address order of the
+          // additions is fixed: deterministic.
 #pragma unroll
-          for (int c8 = 0; c8 < H / 8; c8 += 3) {
-            float4 acc[6];
+          for (int c8 = 0; c8 < H / 8; ++c8) {
+            float f[8];
 #pragma unroll
-            for (int e = 0; e < 3; ++e)
-              if (c8 + e < H / 8) {
-                acc[2 * e] = wp[2 * (c8 + e)];
-                acc[2 * e + 1] = wp[2 * (c8 + e) + 1];
-              }
-#pragma unroll
-            for (int e = 0; e < 3; ++e)
-              if (c8 + e < H / 8) {
-                float f[8];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                  const float2 v = bunpack2<T>(pk[4 * (c8 + e) + t]);
-                  f[2 * t] = v.x * is;
-                  f[2 * t + 1] = v.y * is;
-                }
-                acc[2 * e] = make_float4(acc[2 * e].x + f[0], acc[2 * e].y + f[1], acc[2 * e].z + f[2], acc[2 * e].w + f[3]);
-                acc[2 * e + 1] = make_float4(acc[2 * e + 1].x + f[4], acc[2 * e + 1].y + f[5],
-                                             acc[2 * e + 1].z + f[6], acc[2 * e + 1].w + f[7]);
-                wp[2 * (c8 + e)] = acc[2 * e];
-                wp[2 * (c8 + e) + 1] = acc[2 * e + 1];
-              }
+            for (int t = 0; t < 4; ++t) {
+              const float2 v = bunpack2<T>(pk[4 * c8 + t]);
+              f[2 * t] = v.x * is;
+              f[2 * t + 1] = v.y * is;
+            }
+            atomicAdd(wp + 2 * c8, make_float4(f[0], f[1], f[2], f[3]));
+            atomicAdd(wp + 2 * c8 + 1, make_float4(f[4], f[5], f[6], f[7]));
           }
         }
       }
