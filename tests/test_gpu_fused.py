@@ -129,3 +129,33 @@ def test_swin_block_end_to_end_matches_torch(shift):
     assert (y - y_ref).abs().max().item() <= 3e-2 * y_ref.abs().max().item()
     for got, want in zip((dx, qkv_lin.weight.grad, proj.weight.grad, table.grad), grads_ref):
         assert (got - want).abs().max().item() <= 3e-2 * max(1e-3, want.abs().max().item())
+
+
+@pytest.mark.parametrize("shift", [0, 6])
+def test_swin_b_block_window12_matches_torch(shift):
+    """Swin-B geometry (window 12, L = 144, d = 32): the flat-row kernels with bias/mask/dBias."""
+    torch.manual_seed(1)
+    B, H, W, C, heads, k = 2, 24, 24, 128, 4, 12
+    qkv_lin = torch.nn.Linear(C, 3 * C).cuda()
+    proj = torch.nn.Linear(C, C).cuda()
+    table = torch.nn.Parameter(0.02 * torch.randn((2 * k - 1) ** 2, heads, device="cuda"))
+    x = torch.randn(B, H, W, C, device="cuda", requires_grad=True)
+    mask = ops.shift_mask(H, W, k, shift) if shift else None
+
+    ref = SwinWindowAttentionRef(C, heads, k, shift, qkv_lin, proj, table)
+    y_ref = ref(x, mask)
+    g = torch.randn_like(y_ref)
+    (y_ref * g).sum().backward()
+    grads_ref = [t.grad.clone() for t in (x, qkv_lin.weight, proj.weight, table)]
+    for t in (x, qkv_lin.weight, proj.weight, table):
+        t.grad = None
+
+    xw = fwa.partition_windows(x, k, shift)
+    qkv = qkv_lin(xw).to(torch.bfloat16).contiguous()
+    bias = fwa.relative_position_bias(table, k)
+    o = fwa.window_attention_qkv(qkv, heads, None, bias, mask)
+    y = fwa.reverse_windows(proj(o.float()), k, H, W, shift)
+    (y * g).sum().backward()
+    assert (y - y_ref).abs().max().item() <= 3e-2 * y_ref.abs().max().item()
+    for got, want in zip((x.grad, qkv_lin.weight.grad, proj.weight.grad, table.grad), grads_ref):
+        assert (got - want).abs().max().item() <= 3e-2 * max(1e-3, want.abs().max().item())
