@@ -288,27 +288,42 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
         mbar_arrive(&bars->s_empty);
         float mx = -INFINITY;
         if constexpr (ADD) {
-          // t = scale*log2e*S + (bias+mask)*log2e, kept in s[]
+          // t = scale*log2e*S + (bias+mask)*log2e, kept in s[] (packed f32x2 FMA)
+          const float2 sc2 = make_float2(scale_log2, scale_log2);
 #pragma unroll
-          for (int j = 0; j < 64; ++j) {
-            const float t0 = fmaf(__uint_as_float(s[j]), scale_log2, __uint_as_float(ad[j]));
-            s[j] = __float_as_uint(t0);
-            if (j < L) mx = fmaxf(mx, t0);
+          for (int j = 0; j < 64; j += 2) {
+            const float2 t2 = __ffma2_rn(make_float2(__uint_as_float(s[j]), __uint_as_float(s[j + 1])), sc2,
+                                         make_float2(__uint_as_float(ad[j]), __uint_as_float(ad[j + 1])));
+            s[j] = __float_as_uint(t2.x);
+            s[j + 1] = __float_as_uint(t2.y);
+            if (j + 1 < L) mx = fmaxf(mx, fmaxf(t2.x, t2.y));
+            else if (j < L) mx = fmaxf(mx, t2.x);
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (j < L) mx = fmaxf(mx, __uint_as_float(s[j]));
+          for (int j = 0; j < 64; j += 2) {
+            if (j + 1 < L) {
+              float m3;
+              asm("max.f32 %0, %1, %2, %3;" : "=f"(m3) : "f"(mx), "f"(__uint_as_float(s[j])), "f"(__uint_as_float(s[j + 1])));
+              mx = m3;
+            } else if (j < L) {
+              mx = fmaxf(mx, __uint_as_float(s[j]));
+            }
+          }
         }
         const float mxs = ADD ? mx : mx * scale_log2;
         const float sl2 = ADD ? 1.f : scale_log2;
-        float sum = 0.f;
+        float2 sum2 = make_float2(0.f, 0.f);
+        const float2 sl22 = make_float2(sl2, sl2), nm2 = make_float2(-mxs, -mxs);
         uint32_t pk[32];
 #pragma unroll
         for (int j = 0; j < 64; j += 2) {
-          const float p0 = j < L ? ex2(fmaf(__uint_as_float(s[j]), sl2, -mxs)) : 0.f;
-          const float p1 = j + 1 < L ? ex2(fmaf(__uint_as_float(s[j + 1]), sl2, -mxs)) : 0.f;
-          sum += p0 + p1;
+          // packed f32x2 math; a quarter of the exponentials on the FMA pipe (poly)
+          const float2 a = __ffma2_rn(make_float2(__uint_as_float(s[j]), __uint_as_float(s[j + 1])), sl22, nm2);
+          float2 pp = (j & 7) == 6 ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
+          const float p0 = j < L ? pp.x : 0.f;
+          const float p1 = j + 1 < L ? pp.y : 0.f;
+          sum2 = __fadd2_rn(sum2, make_float2(p0, p1));
           if constexpr (kBF16) {
             __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
             pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
@@ -317,7 +332,7 @@ fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
             pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
           }
         }
-        inv_cur = __frcp_rn(sum);
+        inv_cur = __frcp_rn(sum2.x + sum2.y);
         // P(i) -> TMEM (own unit's 32 columns) once PV(i-1) has consumed P(i-1)
         if (i > 0) {
           mbar_wait(&bars->pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
