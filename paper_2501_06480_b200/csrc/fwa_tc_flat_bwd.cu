@@ -100,7 +100,8 @@ struct BFCfg {
   static constexpr int kKVSlot = (kKVBytes + 1023) / 1024 * 1024;
   // dS buffers: 1 (K/V and Q/dO prefetch depth measured to matter more) or 2
   static constexpr int kDSB = 1;
-  static constexpr int kBase = 1024 + (1 + kDSB) * kPBytes + kTile + 4096;   // sP, sDS[kDSB], staging
+  // sP, sDS[kDSB], staging, + 5 KB: row partials, barriers, lane-mask table
+  static constexpr int kBase = 1024 + (1 + kDSB) * kPBytes + kTile + 5120;
   // units touched between the oldest block with pending gradients and the newest S
   static constexpr int kNeedKV = span_units(L, 2 * kRows);
   // Q/dO stages: 3 when the K/V ring still holds kNeedKV units (the Q/dO slot of block b+2
@@ -259,6 +260,9 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   uint8_t* sSt = sV + KS * C::kKVSlot;               // dQ / dK / dV store staging
   float* red = reinterpret_cast<float*>(sSt + C::kTile);    // [3][2][128] row partials
   BFBarriers* bars = reinterpret_cast<BFBarriers*>(red + 3 * 2 * 128);
+  // disable-output-lane masks for lane ranges [16a, 16b): segment bounds are multiples of 16
+  // (L % 16 == 0), so the MMA warp looks them up instead of recomputing them per MMA chain
+  uint4* lmtab = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(bars + 1) + 15) & ~uintptr_t(15));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -297,6 +301,10 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     tma_prefetch_desc(&tm_do);
   }
   if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
+  for (int t = threadIdx.x; t < 81; t += kBThreads) {
+    const int lo = (t / 9) * 16, hi = (t % 9) * 16;
+    lmtab[t] = make_uint4(blane_off(0, lo, hi), blane_off(1, lo, hi), blane_off(2, lo, hi), blane_off(3, lo, hi));
+  }
   if constexpr (DBIAS) {
     griddep_wait();   // the slice may still be read by the previous call's reduction
     float4* z = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.heads * L * L);
@@ -360,8 +368,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const uint32_t q0 = smem_u32(sQD + qs * 2 * C::kTile), do0 = q0 + C::kTile;
         for (int u = u0; u <= u1; ++u) {
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
-          const uint32_t m0 = blane_off(0, lo, hi), m1 = blane_off(1, lo, hi);
-          const uint32_t m2 = blane_off(2, lo, hi), m3 = blane_off(3, lo, hi);
+          const uint4 mm = lmtab[(lo >> 4) * 9 + (hi >> 4)];
+          const uint32_t m0 = mm.x, m1 = mm.y, m2 = mm.z, m3 = mm.w;
           const uint64_t a_q = make_sdesc(q0, 16, sbo, C::kSwz);
           const uint64_t b_k = make_sdesc(smem_u32(sK + kslot(u) * C::kKVSlot), 16, sbo, C::kSwz);
           if (elect_one()) {
@@ -379,8 +387,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 #endif
         for (int u = u0; u <= u1; ++u) {
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
-          const uint32_t m0 = blane_off(0, lo, hi), m1 = blane_off(1, lo, hi);
-          const uint32_t m2 = blane_off(2, lo, hi), m3 = blane_off(3, lo, hi);
+          const uint4 mm = lmtab[(lo >> 4) * 9 + (hi >> 4)];
+          const uint32_t m0 = mm.x, m1 = mm.y, m2 = mm.z, m3 = mm.w;
           const uint64_t a_do = make_sdesc(do0, 16, sbo, C::kSwz);
           const uint64_t b_v = make_sdesc(smem_u32(sV + kslot(u) * C::kKVSlot), 16, sbo, C::kSwz);
           if (elect_one()) {
@@ -405,8 +413,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         MMA_FENCE_AFTER();
         for (int u = u0; u <= u1; ++u) {
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
-          const uint32_t m0 = blane_off(0, lo, hi), m1 = blane_off(1, lo, hi);
-          const uint32_t m2 = blane_off(2, lo, hi), m3 = blane_off(3, lo, hi);
+          const uint4 mm = lmtab[(lo >> 4) * 9 + (hi >> 4)];
+          const uint32_t m0 = mm.x, m1 = mm.y, m2 = mm.z, m3 = mm.w;
           const uint64_t a_ds = make_sdesc(ds0 + (c % C::kDSB) * C::kPBytes, 16, 256, 6);
           const uint64_t b_k = make_sdesc(smem_u32(sK + kslot(u) * C::kKVSlot), C::kKVSlot, sbo, C::kSwz);
           if (elect_one()) {
