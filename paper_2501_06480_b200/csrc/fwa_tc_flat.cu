@@ -55,9 +55,6 @@ using namespace sm100;
 // warps: 0 producer, 1 S issuer, 2..9 softmax (+ epilogue unless split), 10 PV issuer,
 // 11..14 epilogue (split mode)
 constexpr int kRows = 128;
-#ifndef FWA_POLY_FROM
-#define FWA_POLY_FROM 24   // columns [FWA_POLY_FROM, 32) of each 32-column piece use ex2_poly
-#endif
 
 // units intersecting one 128-row block: block starts are multiples of gcd(128, L) inside
 // a unit, so at most ceil((L - g + 128) / L) units.
@@ -90,6 +87,9 @@ struct FCfg {
   static constexpr bool kSplit = 2 * L + 2 * kPW <= 512;
   static constexpr int kNB = kSplit ? 2 : (3 * kBW <= 512 ? 3 : 2);
   static constexpr int kThreads = kSplit ? 480 : 352;
+  // columns [kPolyFrom, 32) of each 32-column piece exponentiate on the FMA pipe (ex2_poly2):
+  // measured best 37.5 % for d <= 32, 25 % for d = 64 (whose PV leaves less FMA slack)
+  static constexpr int kPolyFrom = D >= 64 ? 24 : 20;
   // units resident between the oldest block awaiting PV and the newest S
   static constexpr int kNeedKV = (L - std::gcd(128, L) + (kNB + 1) * kRows + L - 1) / L;
   static constexpr bool kFits = kKVStages >= kNeedKV && kBW <= 256 && kSmem <= 227 * 1024;
@@ -431,7 +431,7 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             // pairs on packed f32x2 FMA; a quarter of the exponentials (columns 24..31 of
             // each piece) on the FMA pipe instead of the MUFU
             const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[t]), __uint_as_float(r[t + 1])), sx2, nm2);
-            const float2 p = t >= FWA_POLY_FROM ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
+            const float2 p = t >= C::kPolyFrom ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
             sum2 = __fadd2_rn(sum2, p);
             pk[t >> 1] = fpack2<T>(p.x, p.y);
           }
