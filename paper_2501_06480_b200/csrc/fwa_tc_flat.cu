@@ -56,12 +56,6 @@ using namespace sm100;
 // 11..14 epilogue (split mode)
 constexpr int kRows = 128;
 
-// units intersecting one 128-row block: block starts are multiples of gcd(128, L) inside
-// a unit, so at most ceil((L - g + 128) / L) units.
-__host__ __device__ constexpr int max_segments(int L) {
-  return (L - std::gcd(128, L) + kRows + L - 1) / L;
-}
-
 template <int D, int L>
 struct FCfg {
   static constexpr int kRowBytes = D * 2;
@@ -73,7 +67,6 @@ struct FCfg {
   static constexpr int kKVAvail = (227 * 1024 - kFixed) / (2 * kKVSlot);
   static constexpr int kKVStages = kKVAvail < 8 ? kKVAvail : 8;
   static constexpr int kSmem = kFixed + kKVStages * 2 * kKVSlot;
-  static constexpr int kMaxSeg = max_segments(L);
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
   static constexpr int kChunks = kRowBytes / 16;
   static constexpr uint32_t kOCol = ((L / 2 + 15) / 16) * 16;

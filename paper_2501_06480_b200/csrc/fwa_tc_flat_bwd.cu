@@ -1,27 +1,34 @@
 // fwa_tc_flat_bwd.cu — "flat-row" backward for large windows (64 < L <= 256, L % 16 == 0,
-// 2L + (2*ceil(L/128)+1)*d <= 512 TMEM columns; e.g. Swin-B 12x12: L = 144, d = 32) on
-// tcgen05 + TMA (sm_100a), f16/bf16, no bias/mask.
+// TMEM 2L + (1 + 3*ceil(L/128))*d <= 512 columns with two dV sets, else one; e.g. Swin-B
+// 12x12: L = 144, d = 32) on tcgen05 + TMA (sm_100a), f16/bf16, optional Swin bias /
+// shifted-window mask / deterministic dBias (d = 32).
 //
 // As in fwa_tc_flat.cu the CTA owns a contiguous unit range and walks its flat
 // [units*L][d] rows in 128-row query blocks that straddle unit boundaries, so every
 // TMEM lane / softmax thread carries a real query row. Per block b (segments = the
-// units it intersects, lane-masked MMAs per segment):
+// units it intersects, lane-masked MMAs per segment; masks from a smem lookup table):
 //
 //   S  = Q_b K_u^T, dP = dO_b V_u^T          TMEM [0, L), [L, 2L)      (SS, N = L)
 //   softmax warps (8: two per lane quarter, each owns half of the row's keys; row
-//   max / sum / rho combined through smem):
-//     p = 2^(S*c - m*c) (unnormalized)        -> smem sP (f16/bf16, SW128 K-major atoms)
+//   max / sum / rho combined through smem; packed f32x2 math, 1/4 of the exponentials
+//   as a polynomial on the FMA pipe):
+//     [bias/mask: x = S*c + (bias + mask)*log2e from an f16 table, written back over S]
+//     p = 2^(x - m) (unnormalized)            -> smem sP (16-key 32-byte-swizzle atoms)
 //     dO_b rows scaled by 1/l in place        (so dV += p^T (dO/l) = P^T dO)
 //     rho = sum_j p dP / l, dS = (scale/l) p (dP - rho) -> smem sDS
+//     [dBias: this CTA's [heads][L][L] fp32 slice += dS/scale (vector L2 reductions)]
 //   dV_u += p^T dO'_b, dK_u += dS^T Q_b        M = keys (A read MN-major from sP/sDS),
 //                                              K = the segment's query rows, TMEM accumulators
 //   dQ_b  = dS K_u                             (SS, masked per segment) -> TMEM
 //   4 drain warps: dQ_b per block; dK_u / dV_u when unit u's last rows are done.
 //
 // The MMA warp issues S(b+1), dP(b+1) before the gradient MMAs of block b, so the softmax
-// of b+1 overlaps them. One dK/dV accumulator set: a block that finishes unit u and starts
-// u+1 issues u's gradients, commits them for draining, issues dQ_b (covering the drain) and
-// only then starts u+1. HBM: Q, K, V, dO read once; dQ, dK, dV written once (7 L d per unit).
+// of b+1 overlaps them. dV has two accumulator sets (unit parity) when TMEM allows, so all
+// dV MMAs of a block go first and release sP early; dK has one set: a block that finishes
+// unit u and starts u+1 issues u's dK, commits it for draining, issues dQ_b (covering the
+// drain) and only then starts u+1. HBM: Q, K, V, dO read once; dQ, dK, dV written once
+// (7 L d per unit). Timing-experiment builds: -DFWA_TRACE (phase stamps of CTA 0),
+// -DFWA_TC_ONLY (softmax math skipped), -DFWA_NO_DRAIN, -DFWA_PROBE, -DFWA_NO_MMA_FENCE.
 #include <cuda.h>
 #include <math.h>
 
