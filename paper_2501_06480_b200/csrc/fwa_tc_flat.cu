@@ -1,5 +1,6 @@
 // fwa_tc_flat.cu — "flat-row" forward for large windows (64 < L <= 256, L % 16 == 0; e.g.
-// Swin-B 12x12 = 144, 16x16 = 256) on tcgen05 + TMA (sm_100a), f16/bf16, no bias/mask.
+// Swin-B 12x12 = 144, 16x16 = 256) on tcgen05 + TMA (sm_100a), f16/bf16, optional Swin
+// bias / shifted-window mask.
 //
 // For the [units][L][d] layout the units are contiguous, so Q/K/V/O are one flat
 // [units*L][d] row matrix. Each CTA owns a contiguous unit range [ua, ub) and walks
@@ -10,17 +11,21 @@
 //
 //   S = Q_blk K_u^T   one lane-masked SS MMA chain per unit segment (lanes of the
 //                     segment written; tcgen05 disable-output-lane mask), N = L
-//   softmax           thread = row = TMEM lane; pass 1 row max, pass 2 ex2 + row sum,
-//                     P (16-bit pairs) written over the consumed S columns
-//   O = P V_u         lane-masked TS MMA chain per segment (A = P in TMEM), N = d,
-//                     into the S buffer's upper half (O_col = round_up(L/2, 16))
+//   softmax           thread = row = TMEM lane; pass 1 row max (with bias/mask: x = S*c +
+//                     add, add read once from an f16 table and written back over S),
+//                     pass 2 exp2 + row sum (packed f32x2; 3/8 of the exponentials as a
+//                     polynomial on the FMA pipe for d <= 32), P as 16-bit pairs in TMEM
+//   O = P V_u         lane-masked TS MMA chain per segment (A = P in TMEM), N = d
 //   epilogue          1/rowsum, convert, swizzled staging, TMA store (a CTA's last
 //                     block stores 16-row pieces so it never touches the next range)
 //
-// Two 256-column TMEM buffers and two softmax warpgroups ping-pong on alternate blocks:
-// the MMA warp issues S(b+1) before PV(b), so one group's softmax overlaps the other's
-// MMAs and epilogue. K/V of a unit are loaded once into a ring and released after the
-// PV of the last block that touches the unit. HBM: Q, K, V read once, O written once.
+// S and PV are issued from separate warps (S(b) as soon as its TMEM slot is free, PV(b) as
+// soon as the softmax publishes P) and two softmax warpgroups alternate blocks. For L up to
+// ~150 the TMEM is split into two S slots and two P/O slots: the S slot frees as soon as
+// the softmax has read it and a separate epilogue warpgroup drains O; larger L use two or
+// three 256-column buffers with P and O inside the consumed S columns. K/V of a unit are
+// loaded once into a ring and released after the PV of the last block that touches the
+// unit. HBM: Q, K, V read once, O written once.
 #include <cuda.h>
 #include <math.h>
 
