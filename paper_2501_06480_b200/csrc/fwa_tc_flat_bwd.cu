@@ -122,18 +122,22 @@ struct BFCfg {
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
   static constexpr int kChunks = kRowBytes / 16;
   // TMEM columns: S, dP, dQ, dV (two sets, by unit parity, when they fit), dK
-  static constexpr bool kDV2 = 2 * L + D + 3 * kNKT * D <= 512;
+  // S and dP in their own columns when they fit; else (L = 192..256) dP reuses the S columns
+  // once the softmax has read S (one extra MMA latency per block)
+  static constexpr bool kSharedSdP = 2 * L + D + 2 * kNKT * D > 512;
+  static constexpr int kSdP = kSharedSdP ? L : 2 * L;
+  static constexpr bool kDV2 = kSdP + D + 3 * kNKT * D <= 512;
   static constexpr int kVSets = kDV2 ? 2 : 1;
-  static constexpr uint32_t kTS = 0, kTDP = L, kTDQ = 2 * L;
-  static constexpr uint32_t kTDV = 2 * L + D, kTDK = 2 * L + D + kVSets * kNKT * D;
-  static constexpr int kCols = 2 * L + D + (kVSets + 1) * kNKT * D;
+  static constexpr uint32_t kTS = 0, kTDP = kSharedSdP ? 0 : L, kTDQ = kSdP;
+  static constexpr uint32_t kTDV = kSdP + D, kTDK = kSdP + D + kVSets * kNKT * D;
+  static constexpr int kCols = kSdP + D + (kVSets + 1) * kNKT * D;
   static constexpr bool kFits = (L % 16 == 0) && kCols <= 512 && kKS >= kNeedKV &&
                                 kSmem <= 227 * 1024 && kOver <= kQS * 2 * kTile;
 };
 
 struct BFBarriers {
   uint64_t qd_full[3], qd_empty[3], kv_full[6], kv_empty[6];
-  uint64_t s_full, dp_full, p_ready, ds_ready, p_free, ds_free[2];
+  uint64_t s_full, dp_full, p_ready, ds_ready, p_free, ds_free[2], s_read;
   uint64_t acc_full, acc_free, dq_full, dq_free;
   uint64_t probe;
   uint32_t tmem_base;
@@ -290,6 +294,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->dp_full, 1);
     mbar_init(&bars->p_ready, 256);
+    mbar_init(&bars->s_read, 256);
     mbar_init(&bars->ds_ready, 256);
     mbar_init(&bars->p_free, 1);
     mbar_init(&bars->ds_free[0], 1);
@@ -392,6 +397,10 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 #ifdef FWA_TC_ONLY
         if (lane == 0) BTRACE(4, b);
 #endif
+        if constexpr (C::kSharedSdP) {   // dP goes into the S columns: the softmax must have read S
+          mbar_wait(&bars->s_read, b & 1);
+          MMA_FENCE_AFTER();
+        }
         for (int u = u0; u <= u1; ++u) {
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
           const uint4 mm = lmtab[(lo >> 4) * 9 + (hi >> 4)];
@@ -562,6 +571,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       if (trc) BTRACE(3, b);
 #ifdef FWA_TC_ONLY
       // timing experiment: keep the barrier protocol, skip the math
+      if constexpr (C::kSharedSdP) mbar_arrive(&bars->s_read);
       if (b > 0) mbar_wait(&bars->p_free, (b - 1) & 1);
       mbar_wait(&bars->dp_full, b & 1);
       tc_fence_after();
@@ -613,6 +623,10 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           pk[c * 4 + (t >> 1)] = bpack2<T>(p.x, p.y);
         }
       });
+      if constexpr (C::kSharedSdP) {   // S fully read: its columns may take dP
+        tc_fence_before();
+        mbar_arrive(&bars->s_read);
+      }
       rsum[hf * 128 + r] = s2.x + s2.y;
       // p -> sP once the gradient MMAs of b-1 stopped reading it
       if (b > 0) mbar_wait(&bars->p_free, (b - 1) & 1);
