@@ -22,8 +22,10 @@
 //   dQ_b  = dS K_u                             (SS, masked per segment) -> TMEM
 //   4 drain warps: dQ_b per block; dK_u / dV_u when unit u's last rows are done.
 //
-// The MMA warp issues S(b+1), dP(b+1) before the gradient MMAs of block b, so the softmax
-// of b+1 overlaps them. dV has two accumulator sets (unit parity) when TMEM allows, so all
+// Two warps issue the MMAs: one S(b), dP(b) as soon as block b-1's softmax has released the
+// S/dP columns, the other the gradient MMAs of each block as soon as its P and dS are in
+// smem (one issue stream was the measured bottleneck), so the softmax of b+1 overlaps the
+// gradients of b. dV has two accumulator sets (unit parity) when TMEM allows, so all
 // dV MMAs of a block go first and release sP early; dK has one set: a block that finishes
 // unit u and starts u+1 issues u's dK, commits it for draining, issues dQ_b (covering the
 // drain) and only then starts u+1. HBM: Q, K, V, dO read once; dQ, dK, dV written once
@@ -83,7 +85,8 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kBThreads = 448;  // producer, MMA, 8 softmax warps, 4 drain warps
+// warps: 0 producer, 1 S/dP issuer, 2..9 softmax, 10..13 drain, 14 gradient-MMA issuer
+constexpr int kBThreads = 480;
 constexpr int kRows = 128;
 
 __host__ __device__ constexpr int span_units(int L, int rows) {
@@ -117,7 +120,7 @@ struct BFCfg {
   static constexpr int kFixed = kBase + kQS * 2 * kTile;
   static constexpr int kKVAvail = (227 * 1024 - kFixed) / (2 * kKVSlot);
   static constexpr int kKS = kKVAvail < 6 ? kKVAvail : 6;
-  static_assert(kDSB == 1 || kDSB == 2, "dS buffers");
+  static_assert(kDSB == 1, "two dS buffers need the ds_ready aliasing guard (single issuing warp)");
   static constexpr int kSmem = kFixed + kKS * 2 * kKVSlot;
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
   static constexpr int kChunks = kRowBytes / 16;
@@ -353,7 +356,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         tma_load_3d(sQD + qs * 2 * C::kTile + C::kTile, &tm_do, &bars->qd_full[qs], 0, rs, 0, pol);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 14) {
     // ===== MMA issuer: S(b), dP(b), then the gradients of block b-1 =====
     if (nblk > 0) {
       constexpr uint32_t idS = make_idesc_f16(kBF16, 128, L, false, false);
@@ -449,9 +452,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const int rs = r0 + c * kRows, re = min(rs + kRows, r1);
         const int u0 = rs / L, u1 = (re - 1) / L;
         mbar_wait(&bars->p_ready, c & 1);
-        // ds_ready(c) was already waited by issue_SdP(c+1); waiting again could alias with
-        // phase c+1 now that dS is double-buffered (softmax may run a block ahead)
-        if (c == nblk - 1) mbar_wait(&bars->ds_ready, c & 1);
+        // (with kDSB = 1, ds_ready(c+1) needs ds_free(c), committed below: no phase aliasing)
+        mbar_wait(&bars->ds_ready, c & 1);
         MMA_FENCE_AFTER();
         if (lane == 0) BTRACE(1, c);
         const uint32_t q0 = smem_u32(sQD + qs * 2 * C::kTile), do0 = q0 + C::kTile;
@@ -532,11 +534,14 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         if (lane == 0) BTRACE(14, c);
 #endif
       };
-      for (int b = 0; b < nblk; ++b) {
-        issue_SdP(b);
-        if (b > 0) issue_grads(b - 1);
+      // two issuing warps: S/dP of the next block never queues behind the gradient MMAs
+      // of the previous one in a single instruction stream (ordering between the two is
+      // carried by the barriers: S(b+1) after ds_ready(b), gradients(c) after p/ds_ready(c))
+      if (warp == 1) {
+        for (int b = 0; b < nblk; ++b) issue_SdP(b);
+      } else {
+        for (int c = 0; c < nblk; ++c) issue_grads(c);
       }
-      issue_grads(nblk - 1);
     }
   } else if (warp < 10) {
     // ===== softmax / dS: warp pair (w, w+4) share a lane quarter, each owns half the keys =====
