@@ -29,7 +29,9 @@
 // dV MMAs of a block go first and release sP early; dK has one set: a block that finishes
 // unit u and starts u+1 issues u's dK, commits it for draining, issues dQ_b (covering the
 // drain) and only then starts u+1. HBM: Q, K, V, dO read once; dQ, dK, dV written once
-// (7 L d per unit). Timing-experiment builds: -DFWA_TRACE (phase stamps of CTA 0),
+// (7 L d per unit). K and V share one ring of unit slots; where that ring cannot hold the
+// units in flight (L = 208/256 at d = 32, L = 96/112 at d = 64) V gets its own, shallower
+// ring, released by dP instead of by the gradients. Timing-experiment builds: -DFWA_TRACE (phase stamps of CTA 0),
 // -DFWA_TC_ONLY (softmax math skipped), -DFWA_NO_DRAIN, -DFWA_PROBE, -DFWA_NO_MMA_FENCE.
 #include <cuda.h>
 #include <math.h>
@@ -119,9 +121,15 @@ struct BFCfg {
   static constexpr int kQS = (kBase + 3 * 2 * kTile + kNeedKV * 2 * kKVSlot <= 227 * 1024) ? 3 : 2;
   static constexpr int kFixed = kBase + kQS * 2 * kTile;
   static constexpr int kKVAvail = (227 * 1024 - kFixed) / (2 * kKVSlot);
-  static constexpr int kKS = kKVAvail < 6 ? kKVAvail : 6;
+  // K and V rings: V(u) is read only by dP (freed when the dP of u's last block executed), K(u)
+  // also by dQ of the gradients one block later. Same depth when kNeedKV K/V pairs fit; else
+  // (L = 208/256 at d = 32, L = 96/112 at d = 64) kNeedKV K slots and one block's worth of V
+  static constexpr int kVNeed = span_units(L, kRows);
+  static constexpr bool kSplitKV = kKVAvail < kNeedKV;
+  static constexpr int kKS = kSplitKV ? kNeedKV : (kKVAvail < 6 ? kKVAvail : 6);
+  static constexpr int kVS = kSplitKV ? kVNeed : kKS;
   static_assert(kDSB == 1, "two dS buffers need the ds_ready aliasing guard (single issuing warp)");
-  static constexpr int kSmem = kFixed + kKS * 2 * kKVSlot;
+  static constexpr int kSmem = kFixed + (kKS + kVS) * kKVSlot;
   static constexpr uint32_t kSwz = D == 16 ? 6u : (D == 32 ? 4u : 2u);
   static constexpr int kChunks = kRowBytes / 16;
   // TMEM columns: S, dP, dQ, dV (two sets, by unit parity, when they fit), dK
@@ -134,17 +142,19 @@ struct BFCfg {
   static constexpr uint32_t kTS = 0, kTDP = kSharedSdP ? 0 : L, kTDQ = kSdP;
   static constexpr uint32_t kTDV = kSdP + D, kTDK = kSdP + D + kVSets * kNKT * D;
   static constexpr int kCols = kSdP + D + (kVSets + 1) * kNKT * D;
-  static constexpr bool kFits = (L % 16 == 0) && kCols <= 512 && kKS >= kNeedKV &&
-                                kSmem <= 227 * 1024 && kOver <= kQS * 2 * kTile;
+  static constexpr bool kFits = (L % 16 == 0) && kCols <= 512 && kKS >= kNeedKV && kKS <= 6 &&
+                                kVS <= 6 && kSmem <= 227 * 1024 && kOver <= kQS * 2 * kTile;
 };
 
 struct BFBarriers {
-  uint64_t qd_full[3], qd_empty[3], kv_full[6], kv_empty[6];
+  uint64_t qd_full[3], qd_empty[3], k_full[6], k_empty[6], v_full[6], v_empty[6];
   uint64_t s_full, dp_full, p_ready, ds_ready, p_free, ds_free[2], s_read;
   uint64_t acc_full, acc_free, dq_full, dq_free;
   uint64_t probe;
   uint32_t tmem_base;
 };
+// the 5 KB reserve of kBase: row partials [3][2][128] f32, barriers, 81-entry lane-mask table
+static_assert(3 * 2 * 128 * 4 + sizeof(BFBarriers) + 16 + 81 * 16 <= 5120, "flat bwd smem reserve");
 
 template <typename T>
 __device__ __forceinline__ uint32_t bpack2(float a, float b) {
@@ -261,7 +271,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                 int64_t n_units, float scale, FlatBAdd add) {
   using C = BFCfg<D, L>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
-  constexpr int QS = C::kQS, KS = C::kKS, NKT = C::kNKT;
+  constexpr int QS = C::kQS, KS = C::kKS, VS = C::kVS, NKT = C::kNKT;
   constexpr int H = L / 2;  // keys per softmax thread (one half of the row)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -270,8 +280,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   uint8_t* sDS = sP + C::kPBytes;                    // [kDSB] dS tiles
   uint8_t* sQD = sDS + C::kDSB * C::kPBytes;         // [QS][Q | dO] blocks
   uint8_t* sK = sQD + QS * 2 * C::kTile;             // [KS] K slots
-  uint8_t* sV = sK + KS * C::kKVSlot;                // [KS] V slots
-  uint8_t* sSt = sV + KS * C::kKVSlot;               // dQ / dK / dV store staging
+  uint8_t* sV = sK + KS * C::kKVSlot;                // [VS] V slots
+  uint8_t* sSt = sV + VS * C::kKVSlot;               // dQ / dK / dV store staging
   float* red = reinterpret_cast<float*>(sSt + C::kTile);    // [3][2][128] row partials
   BFBarriers* bars = reinterpret_cast<BFBarriers*>(red + 3 * 2 * 128);
   // disable-output-lane masks for lane ranges [16a, 16b): segment bounds are multiples of 16
@@ -291,8 +301,12 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       mbar_init(&bars->qd_empty[s], 1);
     }
     for (int s = 0; s < KS; ++s) {
-      mbar_init(&bars->kv_full[s], 1);
-      mbar_init(&bars->kv_empty[s], 1);
+      mbar_init(&bars->k_full[s], 1);
+      mbar_init(&bars->k_empty[s], 1);
+    }
+    for (int s = 0; s < VS; ++s) {
+      mbar_init(&bars->v_full[s], 1);
+      mbar_init(&bars->v_empty[s], 1);
     }
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->dp_full, 1);
@@ -341,19 +355,26 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       for (int b = 0; b < nblk; ++b) {
         const int rs = r0 + b * kRows;
         const int last = (min(rs + kRows, r1) - 1) / L - (int)ua;
-        for (; next <= last && next < n_loc; ++next) {
+        const int first = next;
+        for (; next <= last && next < n_loc; ++next) {   // K first: S(b) needs Q and K only
           const int s = next % KS;
-          mbar_wait(&bars->kv_empty[s], ((next / KS) & 1) ^ 1);
-          mbar_arrive_expect_tx(&bars->kv_full[s], 2 * C::kKVBytes);
-          const int row = (int)((ua + next) * L);
-          tma_load_3d(sK + s * C::kKVSlot, &tm_k, &bars->kv_full[s], 0, row, 0, pol);
-          tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->kv_full[s], 0, row, 0, pol);
+          mbar_wait(&bars->k_empty[s], ((next / KS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bars->k_full[s], (C::kSplitKV ? 1 : 2) * C::kKVBytes);
+          tma_load_3d(sK + s * C::kKVSlot, &tm_k, &bars->k_full[s], 0, (int)((ua + next) * L), 0, pol);
+          if constexpr (!C::kSplitKV)   // one ring: V rides on K's barriers (measured faster)
+            tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->k_full[s], 0, (int)((ua + next) * L), 0, pol);
         }
         const int qs = b % QS;
         mbar_wait(&bars->qd_empty[qs], ((b / QS) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->qd_full[qs], 2 * C::kTile);
         tma_load_3d(sQD + qs * 2 * C::kTile, &tm_q, &bars->qd_full[qs], 0, rs, 0, pol);
         tma_load_3d(sQD + qs * 2 * C::kTile + C::kTile, &tm_do, &bars->qd_full[qs], 0, rs, 0, pol);
+        for (int u = first; C::kSplitKV && u < next; ++u) {   // V free once dP of u's last block ran
+          const int s = u % VS;
+          mbar_wait(&bars->v_empty[s], ((u / VS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bars->v_full[s], C::kKVBytes);
+          tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->v_full[s], 0, (int)((ua + u) * L), 0, pol);
+        }
       }
     }
   } else if (warp == 1 || warp == 14) {
@@ -368,6 +389,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       uint32_t probe_ph = 0;
       (void)probe_ph;
       auto kslot = [&](int u) { return (u - (int)ua) % KS; };
+      auto vslot = [&](int u) { return (u - (int)ua) % VS; };
       auto issue_SdP = [&](int b) {
         const int qs = b % QS;
         const int rs = r0 + b * kRows, re = min(rs + kRows, r1);
@@ -375,7 +397,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         mbar_wait(&bars->qd_full[qs], (b / QS) & 1);
         for (int u = u0; u <= u1; ++u) {
           const int lu = u - (int)ua;
-          mbar_wait(&bars->kv_full[lu % KS], (lu / KS) & 1);
+          mbar_wait(&bars->k_full[lu % KS], (lu / KS) & 1);
         }
         if (b > 0) mbar_wait(&bars->ds_ready, (b - 1) & 1);   // S / dP of b-1 consumed
         MMA_FENCE_AFTER();
@@ -400,16 +422,22 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 #ifdef FWA_TC_ONLY
         if (lane == 0) BTRACE(4, b);
 #endif
+        if constexpr (C::kSplitKV) {
+          for (int u = u0; u <= u1; ++u) {
+            const int lu = u - (int)ua;
+            mbar_wait(&bars->v_full[lu % VS], (lu / VS) & 1);
+          }
+        }
         if constexpr (C::kSharedSdP) {   // dP goes into the S columns: the softmax must have read S
           mbar_wait(&bars->s_read, b & 1);
-          MMA_FENCE_AFTER();
         }
+        if constexpr (C::kSplitKV || C::kSharedSdP) MMA_FENCE_AFTER();
         for (int u = u0; u <= u1; ++u) {
           const int lo = max(u * L, rs) - rs, hi = min((u + 1) * L, re) - rs;
           const uint4 mm = lmtab[(lo >> 4) * 9 + (hi >> 4)];
           const uint32_t m0 = mm.x, m1 = mm.y, m2 = mm.z, m3 = mm.w;
           const uint64_t a_do = make_sdesc(do0, 16, sbo, C::kSwz);
-          const uint64_t b_v = make_sdesc(smem_u32(sV + kslot(u) * C::kKVSlot), 16, sbo, C::kSwz);
+          const uint64_t b_v = make_sdesc(smem_u32(sV + vslot(u) * C::kKVSlot), 16, sbo, C::kSwz);
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk)
@@ -418,7 +446,14 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           }
           __syncwarp();
         }
-        if (elect_one()) mma_commit(&bars->dp_full);
+        if (elect_one()) {
+          mma_commit(&bars->dp_full);
+          // V of the units whose last rows were in this block: read by nothing after this dP
+          if constexpr (C::kSplitKV) {
+            const int nxt_u0 = (b + 1 < nblk) ? (rs + kRows) / L : u1 + 1;
+            for (int u = u0; u <= u1 && u < nxt_u0; ++u) mma_commit(&bars->v_empty[vslot(u)]);
+          }
+        }
         __syncwarp();
 #ifdef FWA_TC_ONLY
         if (lane == 0) BTRACE(5, b);
@@ -525,7 +560,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           if constexpr (!C::kDV2) mma_commit(&bars->p_free);
           mma_commit(&bars->ds_free[c % C::kDSB]);
           mma_commit(&bars->qd_empty[qs]);
-          for (int u = u0; u <= u1 && u < nxt_u0; ++u) mma_commit(&bars->kv_empty[kslot(u)]);
+          for (int u = u0; u <= u1 && u < nxt_u0; ++u) mma_commit(&bars->k_empty[kslot(u)]);
         }
         __syncwarp();
         if (lane == 0) BTRACE(2, c);

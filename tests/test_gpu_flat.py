@@ -63,6 +63,8 @@ def _ref_bwd(q, k, v, do, scale):
     (149, 144, 32), (301, 144, 32), (1000, 144, 32), (150, 80, 32), (151, 96, 16), (149, 112, 32),
     (148, 128, 32), (297, 160, 32), (160, 176, 32), (149, 208, 16), (150, 128, 64), (7, 144, 32),
     (1, 144, 32), (149, 256, 16), (149, 192, 32), (150, 240, 32), (151, 224, 16),
+    # split K / V rings (kNeedKV K slots, one block's worth of V)
+    (149, 256, 32), (1, 256, 32), (3, 256, 32), (151, 208, 32), (150, 96, 64), (149, 112, 64),
 ])
 def test_flat_backward_matches_fp32(dt, units, L, d):
     rng = fwa.Rng(units * 17 + L + d)
