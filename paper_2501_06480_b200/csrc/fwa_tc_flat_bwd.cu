@@ -732,26 +732,32 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       mbar_arrive(&bars->ds_ready);
       if (trc) BTRACE(6, b);
       if constexpr (DBIAS) {
-        // dBias partial: += dS / scale = P (dP - rho), rows of this CTA's range only
-        if (r0 + b * kRows + r < r1) {
-          float4* wp = reinterpret_cast<float4*>(add.ws + ((size_t)blockIdx.x * add.heads + hrow) * L * L +
-                                                 (size_t)irow * L + hf * H);
-          const float is = 1.f / scale;
-          // fire-and-forget vector reductions (no load round trip). One thread owns a
-          // [head][query] row of this CTA's slice per block and consecutive blocks are
-          // separated by the softmax warpgroup's barriers, so the per-address order of the
-          // additions is fixed: deterministic.
+        // dBias partial: += dS / scale = P (dP - rho), rows of this CTA's range only, read
+        // back from sDS so that a warp's vector reductions cover 8 rows x 64 contiguous bytes
+        // (16 full 32-byte sectors per instruction; one row per lane, each lane on its own
+        // half sector, measured 1.9x slower in L2: tools/micro/red_rate.cu). Each warp owns
+        // 16 rows; per address one thread per block, and consecutive blocks are separated by
+        // the softmax warpgroup's barriers: the order of the additions is fixed
+        // (deterministic).
+        named_sync(1, 256);   // every row of dS(b) in sDS
+        const int wq = warp - 2, rr = lane & 7;
+        const float is = 1.f / scale;
+        const float2 is2 = make_float2(is, is);
+        float4* slice = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.heads * L * L);
 #pragma unroll
-          for (int c8 = 0; c8 < H / 8; ++c8) {
-            float f[8];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const float2 v = bunpack2<T>(pk[4 * c8 + t]);
-              f[2 * t] = v.x * is;
-              f[2 * t + 1] = v.y * is;
+        for (int grp = 0; grp < 2; ++grp) {
+          const int lr = wq * 16 + grp * 8 + rr;   // block row
+          const int g = r0 + b * kRows + lr;
+          if (g < r1) {
+            const int u = g / L, i = g - (g / L) * L;
+            float4* wp = slice + ((u % add.heads) * L + i) * (L / 4);
+#pragma unroll 3
+            for (int it = 0; it < L / 16; ++it) {
+              const int c = it * 4 + (lane >> 3);   // 4-key column (float4 of the slice row)
+              const uint2 w = *reinterpret_cast<const uint2*>(sDSb + patom_off(lr, c * 4) + (c & 1) * 8);
+              const float2 a = __fmul2_rn(bunpack2<T>(w.x), is2), e = __fmul2_rn(bunpack2<T>(w.y), is2);
+              atomicAdd(wp + c, make_float4(a.x, a.y, e.x, e.y));
             }
-            atomicAdd(wp + 2 * c8, make_float4(f[0], f[1], f[2], f[3]));
-            atomicAdd(wp + 2 * c8 + 1, make_float4(f[4], f[5], f[6], f[7]));
           }
         }
       }
