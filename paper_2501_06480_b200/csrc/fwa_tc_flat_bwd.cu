@@ -149,7 +149,7 @@ struct BFCfg {
 struct BFBarriers {
   uint64_t qd_full[3], qd_empty[3], k_full[6], k_empty[6], v_full[6], v_empty[6];
   uint64_t s_full, dp_full, p_ready, ds_ready, p_free, ds_free[2], s_read;
-  uint64_t acc_full, acc_free, dq_full, dq_free;
+  uint64_t acc_full, acc_free, dq_full, dq_free, dsr_free;
   uint64_t probe;
   uint32_t tmem_base;
 };
@@ -320,6 +320,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     mbar_init(&bars->acc_free, 128);
     mbar_init(&bars->dq_full, 1);
     mbar_init(&bars->dq_free, 128);
+    mbar_init(&bars->dsr_free, 128);
     mbar_init(&bars->probe, 1);
     fence_mbar_init();
   }
@@ -721,6 +722,9 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       });
       tc_fence_before();   // S / dP reads done before ds_ready lets S(b+1) overwrite them
       if (b >= C::kDSB) mbar_wait(&bars->ds_free[b % C::kDSB], ((b / C::kDSB) - 1) & 1);   // buffer read
+      if constexpr (DBIAS) {   // ... and by the drain warps' dBias reductions
+        if (b > 0) mbar_wait(&bars->dsr_free, (b - 1) & 1);
+      }
       uint8_t* sDSb = sDS + (b % C::kDSB) * C::kPBytes;
 #pragma unroll
       for (int c8 = 0; c8 < H / 8; ++c8) {
@@ -731,36 +735,6 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       fence_proxy_async_smem();
       mbar_arrive(&bars->ds_ready);
       if (trc) BTRACE(6, b);
-      if constexpr (DBIAS) {
-        // dBias partial: += dS / scale = P (dP - rho), rows of this CTA's range only, read
-        // back from sDS so that a warp's vector reductions cover 8 rows x 64 contiguous bytes
-        // (16 full 32-byte sectors per instruction; one row per lane, each lane on its own
-        // half sector, measured 1.9x slower in L2: tools/micro/red_rate.cu). Each warp owns
-        // 16 rows; per address one thread per block, and consecutive blocks are separated by
-        // the softmax warpgroup's barriers: the order of the additions is fixed
-        // (deterministic).
-        named_sync(1, 256);   // every row of dS(b) in sDS
-        const int wq = warp - 2, rr = lane & 7;
-        const float is = 1.f / scale;
-        const float2 is2 = make_float2(is, is);
-        float4* slice = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.heads * L * L);
-#pragma unroll
-        for (int grp = 0; grp < 2; ++grp) {
-          const int lr = wq * 16 + grp * 8 + rr;   // block row
-          const int g = r0 + b * kRows + lr;
-          if (g < r1) {
-            const int u = g / L, i = g - (g / L) * L;
-            float4* wp = slice + ((u % add.heads) * L + i) * (L / 4);
-#pragma unroll 3
-            for (int it = 0; it < L / 16; ++it) {
-              const int c = it * 4 + (lane >> 3);   // 4-key column (float4 of the slice row)
-              const uint2 w = *reinterpret_cast<const uint2*>(sDSb + patom_off(lr, c * 4) + (c & 1) * 8);
-              const float2 a = __fmul2_rn(bunpack2<T>(w.x), is2), e = __fmul2_rn(bunpack2<T>(w.y), is2);
-              atomicAdd(wp + c, make_float4(a.x, a.y, e.x, e.y));
-            }
-          }
-        }
-      }
     }
   } else {
     // ===== drain warps: dK/dV of finished units, dQ of every block =====
@@ -833,8 +807,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       tc_fence_after();
 #ifdef FWA_NO_DRAIN
       mbar_arrive(&bars->dq_free);
-      continue;
-#endif
+#else
       uint32_t gq[D];
 #pragma unroll
       for (int q = 0; q < D / 16; ++q)
@@ -843,7 +816,38 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       tc_fence_before();
       mbar_arrive(&bars->dq_free);
       emit(gq, &tm_dq, &tm_dq16, rs, re - rs);
+#endif
       if (leader) BTRACE(7, b);
+      if constexpr (DBIAS) {
+        // dBias partial of block b: += dS / scale = P (dP - rho) for this CTA's rows, read back
+        // from sDS here, off the softmax's path (it waits dsr_free only before overwriting
+        // sDS with block b+1). A warp's vector reductions cover 8 rows x 64 contiguous bytes:
+        // 16 full 32-byte sectors per instruction (one row per lane, each lane on its own half
+        // sector, measured 1.9x slower in L2: tools/micro/red_rate.cu). Per address one
+        // thread per block, blocks ordered through ds_ready / dsr_free: deterministic.
+        mbar_wait(&bars->ds_ready, b & 1);   // sDS(b) visible (cannot have advanced: dsr_free)
+        const int wq = warp - 10, rr = lane & 7;
+        const float is = 1.f / scale;
+        const float2 is2 = make_float2(is, is);
+        float4* slice = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.heads * L * L);
+#pragma unroll 1
+        for (int grp = 0; grp < 4; ++grp) {
+          const int lr = wq * 32 + grp * 8 + rr;   // block row
+          const int g = rs + lr;
+          if (g < r1) {
+            const int u = g / L, i = g - (g / L) * L;
+            float4* wp = slice + ((u % add.heads) * L + i) * (L / 4);
+#pragma unroll 3
+            for (int it = 0; it < L / 16; ++it) {
+              const int c = it * 4 + (lane >> 3);   // 4-key column (float4 of the slice row)
+              const uint2 w = *reinterpret_cast<const uint2*>(sDS + patom_off(lr, c * 4) + (c & 1) * 8);
+              const float2 a = __fmul2_rn(bunpack2<T>(w.x), is2), e = __fmul2_rn(bunpack2<T>(w.y), is2);
+              atomicAdd(wp + c, make_float4(a.x, a.y, e.x, e.y));
+            }
+          }
+        }
+        mbar_arrive(&bars->dsr_free);
+      }
     }
     if (leader) bulk_wait_read<0>();
   }

@@ -17,6 +17,7 @@ rng = fwa.Rng(1)
 q, k, v, do = (fwa.fill_uniform(rng, (N, h, L, d), dtype=dt) for _ in range(4))
 bias = fwa.fill_uniform(rng, (h, L, L), -0.5, 0.5)
 win = int(round(L ** 0.5))
+assert win * win == L, "square windows only"
 mask = ops.shift_mask(8 * win, 8 * win, win, win // 2)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
