@@ -762,10 +762,20 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       fence_proxy_async_smem();
       named_sync(3, 128);
       if (leader) {
-        if (nrows == kRows) {
-          tma_store_3d(m128, sSt, 0, row0, 0);
+        if constexpr (DBIAS) {   // gradients stream out evict_first: the dBias slices stay in L2
+          const uint64_t spol = policy_evict_first();
+          if (nrows == kRows) {
+            tma_store_3d_hint(m128, sSt, 0, row0, 0, spol);
+          } else {
+            for (int t = 0; t < nrows; t += 16)
+              tma_store_3d_hint(m16, sSt + t * C::kRowBytes, 0, row0 + t, 0, spol);
+          }
         } else {
-          for (int t = 0; t < nrows; t += 16) tma_store_3d(m16, sSt + t * C::kRowBytes, 0, row0 + t, 0);
+          if (nrows == kRows) {
+            tma_store_3d(m128, sSt, 0, row0, 0);
+          } else {
+            for (int t = 0; t < nrows; t += 16) tma_store_3d(m16, sSt + t * C::kRowBytes, 0, row0 + t, 0);
+          }
         }
         bulk_commit();
       }
@@ -829,6 +839,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const int wq = warp - 10, rr = lane & 7;
         const float is = 1.f / scale;
         const float2 is2 = make_float2(is, is);
+        const uint64_t rpol = policy_evict_last();   // 4.3 KB/row slices stay resident in L2
         float4* slice = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.heads * L * L);
 #pragma unroll 1
         for (int grp = 0; grp < 4; ++grp) {
@@ -842,7 +853,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
               const int c = it * 4 + (lane >> 3);   // 4-key column (float4 of the slice row)
               const uint2 w = *reinterpret_cast<const uint2*>(sDS + patom_off(lr, c * 4) + (c & 1) * 8);
               const float2 a = __fmul2_rn(bunpack2<T>(w.x), is2), e = __fmul2_rn(bunpack2<T>(w.y), is2);
-              atomicAdd(wp + c, make_float4(a.x, a.y, e.x, e.y));
+              red_add_v4_hint(wp + c, make_float4(a.x, a.y, e.x, e.y), rpol);
             }
           }
         }
