@@ -291,7 +291,7 @@ def max_over_ranks(torch, dist, x, dev):
     return float(t.item())
 
 
-def flushed_launch_ms(torch, work, i, fwd, bwd, reps=5):
+def flushed_launch_ms(torch, work, i, fwd, bwd, reps=21):
     """Median device time of one layer launch with L2 flushed before it.
 
     The flush READS a 512 MB buffer (a sum), so L2 is refilled with clean lines:
@@ -350,7 +350,7 @@ def measure(args, name, dev, rank, world, dist, steps, with_e2e):
             "algorithmic_bytes_per_launch": mult * unit_bytes,
             "bytes_per_unit": f"{mult}*L*d*{work.eb} = {mult * L * d * work.eb} B",
             "how": "CUDA events around one eager launch on the launching stream, L2 flushed "
-                   "(512 MB read) before each launch, median of 5",
+                   "(512 MB read) before each launch, median of 21",
             "launches": kern,
             "step_frac": byts / (ms_step / 1e3) / 1e9 / peak}
     out = {"value": windows * world / (ms_step / 1e3), "ms_per_step": ms_step,
