@@ -57,8 +57,15 @@ WORKLOADS = {
     "large_sweep": dict(layers=LARGE, batch=1, cpu_div=512, dtype="float16", bwd=False, extras=False, k=8,
                         desc="large-window sweep L=64/256, d=32/64, ~1 GB per call, fp16 "
                              "forward (configs[4])"),
+    "large_sweep_fwdbwd": dict(layers=LARGE, batch=1, cpu_div=512, dtype="float16", bwd=True,
+                               extras=False, k=8,
+                               desc="large-window sweep L=64/256, d=32/64, fp16 forward+backward "
+                                    "(configs[4])"),
 }
 METRIC = "window-attn windows/s + % HBM roofline"
+# measured on the default run beside the headline (configs[2], [3] plain and with training
+# extras, [4] forward and forward+backward)
+EMBEDDED = ("swin_t_fwdbwd", "swin_b_fwdbwd", "swin_b_train", "large_sweep", "large_sweep_fwdbwd")
 
 
 def load_peaks():
@@ -221,11 +228,17 @@ class GpuWorkload:
         torch.cuda.synchronize()
 
     def layer(self, i, fwd=True, bwd=None):
+        """One layer call as the autograd Function runs it: for large windows with bias /
+        mask the (bias + mask) score table is built once and shared by fwd and bwd."""
         q, kk, v, do, bias, mask, o, sc = self.bufs[i]
+        bwd = self.wl["bwd"] if bwd is None else bwd
+        table = self.ops.build_add_table(*q.shape, q.dtype, bias, mask) \
+            if fwd and bwd and (bias is not None or mask is not None) else None
         if fwd:
-            self.ops.attention_forward(q, kk, v, sc, bias, mask, out=o)
-        if self.wl["bwd"] if bwd is None else bwd:
-            self.ops.attention_backward(q, kk, v, do, sc, bias, mask, want_dbias=bias is not None)
+            self.ops.attention_forward(q, kk, v, sc, bias, mask, out=o, add_table=table)
+        if bwd:
+            self.ops.attention_backward(q, kk, v, do, sc, bias, mask, want_dbias=bias is not None,
+                                        add_table=table)
 
     def step(self):
         for i in range(len(self.bufs)):
@@ -460,10 +473,13 @@ def run_gpu(args):
     sampler = ClockSampler(int(vis[local]) if len(vis) > local and vis[local].isdigit() else local)
     sampler.start()
     main_res = measure(args, args.workload, dev, rank, world, dist, args.steps, not args.no_e2e)
-    extra = None
+    # the other BASELINE configs ride on the default run as embedded lines (same method)
+    embedded = {}
     if args.workload == "swin_t_fwd" and not args.no_extra:
-        extra = measure(args, "swin_t_fwdbwd", dev, rank, world, dist, max(3, args.steps // 2),
-                        False)
+        for name in EMBEDDED:
+            embedded[name] = measure(args, name, dev, rank, world, dist,
+                                     max(3, args.steps // 4), False)
+    extra = embedded.get("swin_t_fwdbwd")
     clocks = sampler.stop()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -492,13 +508,19 @@ def run_gpu(args):
             "roofline": main_res["roofline"], "gpu_launches": main_res["gpu_launches"],
             "e2e": main_res.get("e2e"), "cpu_baseline": cpu, "clocks": clocks,
         }
+        def summary(name, res):
+            w = WORKLOADS[name]
+            return {"workload": name, "desc": w["desc"], "value": res["value"],
+                    "unit": "windows/s", "ms_per_step": res["ms_per_step"],
+                    "dtype": {"float16": "f16", "bfloat16": "bf16"}[w["dtype"]],
+                    "hbm_frac_step": res["hbm_frac_step"], "tflops": res["tflops"],
+                    "roofline": res["roofline"], "gpu_launches": res["gpu_launches"],
+                    "layers": [list(x) for x in w["layers"]]}
         if extra is not None:
-            line["fwd_bwd"] = {"workload": "swin_t_fwdbwd",
-                               "desc": WORKLOADS["swin_t_fwdbwd"]["desc"],
-                               "value": extra["value"], "unit": "windows/s",
-                               "ms_per_step": extra["ms_per_step"], "dtype": "bf16",
-                               "hbm_frac_step": extra["hbm_frac_step"], "tflops": extra["tflops"],
-                               "roofline": extra["roofline"], "gpu_launches": extra["gpu_launches"]}
+            line["fwd_bwd"] = summary("swin_t_fwdbwd", extra)
+        if embedded:
+            line["embedded"] = {n: summary(n, r) for n, r in embedded.items()
+                                if n != "swin_t_fwdbwd"}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

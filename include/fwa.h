@@ -2,9 +2,12 @@
  * fwa.h — C-ABI of the B200-native Flash Window Attention library (libfwa.so).
  *
  * Plain pointers and sizes only; no torch or C++ types cross this boundary.
- * Every device pointer is caller-owned (the library never allocates device
- * memory); every call is stream-ordered on the `stream` argument (a
- * cudaStream_t passed as void*), re-entrant, and returns an fwa_status.
+ * Every device pointer is caller-owned: the library never allocates device
+ * memory (scratch comes from the caller's `workspace`, sized by the
+ * fwa_*_workspace_bytes queries) and never changes process-wide CUDA state
+ * (memory pools, limits). Every call is stream-ordered on the `stream`
+ * argument (a cudaStream_t passed as void*), re-entrant and thread-safe
+ * (per-device caches behind a mutex), and returns an fwa_status.
  * On a non-zero status, fwa_last_error() returns a thread-local message.
  *
  * The reference (`flashwin`, pure Python) has no FFI; its "operator API" is
@@ -30,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FWA_ABI_VERSION 1
+#define FWA_ABI_VERSION 2
 
 /* Status codes. The Python layer maps them back onto the reference's
  * exception classes (pkg/src/flashwin/errors.py:4-33). */
@@ -65,7 +68,11 @@ typedef struct {
   int32_t chunks;       /* TileConfig.r: feature chunks, validated like flash.py:57-66 */
   int32_t mask_windows; /* nW of the mask tensor; 0 when mask == NULL */
   int32_t kernel;       /* fwa_kernel */
-  int32_t reserved;
+  int32_t reserved;     /* 0 */
+  /* Optional prebuilt score addend for the large-window kernels: the output of
+   * fwa_build_add_table for this call's bias/mask (e.g. built once per layer and
+   * shared by its forward and backward). NULL = built per call in `workspace`. */
+  const void* add_table;
 } fwa_desc;
 
 /* Per-launch facts (analogue of peak_sram_forward/backward, flash.py:84-95,
@@ -100,21 +107,39 @@ typedef struct {
 /* Forward over all (window, head) units.
  * Replaces flash_forward (flash.py:141-184) and batched_flash_forward
  * (flash.py:269-319): O = softmax(scale*Q K^T [+ bias[h]] [+ mask[n % nW]]) V.
- * Validation (shape/range/capacity) completes before any work is enqueued. */
+ * Validation (shape/range/capacity) completes before any work is enqueued.
+ * `workspace` must hold fwa_fwd_workspace_bytes(desc, bias != NULL, mask != NULL)
+ * bytes (NULL when that is 0: always for L <= 64 or without bias/mask). */
 int fwa_fwd(const fwa_desc* desc, const void* q, const void* k, const void* v,
-            const float* bias, const float* mask, void* o, void* stream);
+            const float* bias, const float* mask, void* o, void* workspace,
+            size_t workspace_bytes, void* stream);
+
+size_t fwa_fwd_workspace_bytes(const fwa_desc* desc, int has_bias, int has_mask);
 
 /* Backward: recomputes P on chip (no O / LSE read), returns dQ, dK, dV and,
- * when dbias != NULL, dBias[h][L][L] = sum_n dS[n,h] (deterministic, no float
- * atomics). Replaces flash_backward (flash.py:187-266).
- * `workspace` must hold fwa_bwd_workspace_bytes(desc) bytes (may be NULL
- * when that is 0). */
+ * when dbias != NULL, dBias[h][L][L] = sum_n dS[n,h]. Replaces flash_backward
+ * (flash.py:187-266). dBias is deterministic (bitwise repeatable): per-CTA
+ * fp32 partials in `workspace`, each address accumulated in a fixed order
+ * (the large-window kernel's vector L2 reductions are issued by one thread
+ * per (block, row) and ordered block after block by the kernel's mbarriers),
+ * then summed over CTAs in ascending order. `workspace` must hold
+ * fwa_bwd_workspace_bytes(desc, bias != NULL, mask != NULL, dbias != NULL)
+ * bytes (may be NULL when that is 0). */
 int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const void* v,
             const void* dout, const float* bias, const float* mask, void* dq,
             void* dk, void* dv, float* dbias, void* workspace,
             size_t workspace_bytes, void* stream);
 
-size_t fwa_bwd_workspace_bytes(const fwa_desc* desc, int want_dbias);
+size_t fwa_bwd_workspace_bytes(const fwa_desc* desc, int has_bias, int has_mask,
+                               int want_dbias);
+
+/* The large-window kernels' score addend (bias[h] + mask[n % nW]) * log2e as f16
+ * [nW][h][L][L]. fwa_add_table_bytes is 0 when no kernel of this shape reads it;
+ * a table built once can be passed to the forward and backward of the same layer
+ * through desc->add_table (saves one build per call). */
+size_t fwa_add_table_bytes(const fwa_desc* desc, int has_bias, int has_mask);
+int fwa_build_add_table(const fwa_desc* desc, const float* bias, const float* mask,
+                        void* table, size_t table_bytes, void* stream);
 
 /* Shape/budget query, no device work (peak_sram_forward/backward + _check_budget,
  * flash.py:84-103). Returns FWA_ERR_CAPACITY when no kernel can run the shape. */
@@ -128,7 +153,8 @@ int fwa_footprint(const fwa_desc* desc, fwa_footprint_t* out);
  * permute copies around window attention disappear. tcgen05 path only
  * (seq_len <= 64, head_dim in {16,32,64}, f16/bf16); FWA_ERR_CAPACITY otherwise. */
 int fwa_fwd_qkv(const fwa_desc* desc, const void* qkv, const float* bias,
-                const float* mask, void* o, void* stream);
+                const float* mask, void* o, void* workspace, size_t workspace_bytes,
+                void* stream);
 
 /* Backward in the same layouts: dout [N][L][h][d] -> dqkv [N][L][3][h][d]. */
 int fwa_bwd_qkv(const fwa_desc* desc, const void* qkv, const void* dout,

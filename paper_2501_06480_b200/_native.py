@@ -58,6 +58,7 @@ class FwaDesc(ctypes.Structure):
         ("mask_windows", ctypes.c_int32),
         ("kernel", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
+        ("add_table", ctypes.c_void_p),
     ]
 
 
@@ -90,18 +91,26 @@ class FwaWinDesc(ctypes.Structure):
 
 _vp = ctypes.c_void_p
 _SIGNATURES = {
-    "fwa_fwd": (ctypes.c_int, [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fwa_fwd": (ctypes.c_int, [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                               ctypes.c_size_t, _vp]),
+    "fwa_fwd_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(FwaDesc), ctypes.c_int,
+                                                  ctypes.c_int]),
+    "fwa_add_table_bytes": (ctypes.c_size_t, [ctypes.POINTER(FwaDesc), ctypes.c_int, ctypes.c_int]),
+    "fwa_build_add_table": (ctypes.c_int, [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, ctypes.c_size_t,
+                                           _vp]),
     "fwa_bwd": (
         ctypes.c_int,
         [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
          ctypes.c_size_t, _vp],
     ),
-    "fwa_fwd_qkv": (ctypes.c_int, [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, _vp, _vp]),
+    "fwa_fwd_qkv": (ctypes.c_int, [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, _vp, _vp,
+                                   ctypes.c_size_t, _vp]),
     "fwa_bwd_qkv": (
         ctypes.c_int,
         [ctypes.POINTER(FwaDesc), _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp],
     ),
-    "fwa_bwd_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(FwaDesc), ctypes.c_int]),
+    "fwa_bwd_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(FwaDesc), ctypes.c_int,
+                                                  ctypes.c_int, ctypes.c_int]),
     "fwa_footprint": (ctypes.c_int, [ctypes.POINTER(FwaDesc), ctypes.POINTER(FwaFootprint)]),
     "fwa_window_partition": (ctypes.c_int, [ctypes.POINTER(FwaWinDesc), _vp, _vp, _vp]),
     "fwa_window_reverse": (ctypes.c_int, [ctypes.POINTER(FwaWinDesc), _vp, _vp, _vp]),

@@ -218,13 +218,35 @@ class BatchedContexts(Sequence):
     def __len__(self):
         return self.B
 
+    @staticmethod
+    def _slice(x, b, hd):
+        """(L, C) slice of one (b, head) in the caller's container type.
+
+        torch tensors and NumPy arrays are views; the reference's DenseTensor (and
+        HostArray) have no ``__getitem__`` (tensor.py:26-71), so objects with an
+        ``.array`` attribute are sliced through it and returned as a read-only
+        HostArray view — which flash_backward accepts like any ``.array`` object.
+        """
+        if isinstance(x, torch.Tensor):
+            return x[b, hd]
+        if hasattr(x, "array"):
+            return HostArray(np.asarray(x.array)[b, hd])
+        return np.asarray(x)[b, hd]
+
     def __getitem__(self, b):
         if isinstance(b, slice):
             return [self[i] for i in range(*b.indices(self.B))]
         if not -self.B <= b < self.B:
             raise IndexError(b)
         b %= self.B
-        return [FlashContext(q=self.q[b, hd], k=self.k[b, hd], v=self.v[b, hd], cfg=self.cfg)
+        # the forward's Swin extras follow the slice: bias[head] and mask[b % nW] (window b
+        # of the batched call uses mask[b % nW]), so flash_backward on one slice
+        # differentiates exactly the attention that batched_flash_forward ran
+        mask = None if self.mask is None else self.mask[b % self.mask.shape[0]]
+        return [FlashContext(q=self._slice(self.q, b, hd), k=self._slice(self.k, b, hd),
+                             v=self._slice(self.v, b, hd), cfg=self.cfg,
+                             bias=None if self.bias is None else self.bias[hd],
+                             mask=mask, mask_windows=0 if mask is None else 1)
                 for hd in range(self.h)]
 
 

@@ -20,18 +20,22 @@ class WindowAttentionFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, bias, mask, scale, kernel):
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-        o = ops.attention_forward(q, k, v, scale, bias, mask, kernel=kernel)
-        ctx.save_for_backward(q, k, v, bias, mask)
+        # large windows: the (bias + mask) score table is built once per layer call and
+        # shared by this forward and its backward (None for L <= 64 / no bias or mask)
+        table = ops.build_add_table(*q.shape, q.dtype, bias, mask, kernel=kernel)
+        o = ops.attention_forward(q, k, v, scale, bias, mask, kernel=kernel, add_table=table)
+        ctx.save_for_backward(q, k, v, bias, mask, table)
         ctx.scale = scale
         ctx.kernel = kernel
         return o
 
     @staticmethod
     def backward(ctx, do):
-        q, k, v, bias, mask = ctx.saved_tensors
+        q, k, v, bias, mask, table = ctx.saved_tensors
         want_db = bias is not None and ctx.needs_input_grad[3]
         dq, dk, dv, db = ops.attention_backward(q, k, v, do.contiguous(), ctx.scale, bias, mask,
-                                                kernel=ctx.kernel, want_dbias=want_db)
+                                                kernel=ctx.kernel, want_dbias=want_db,
+                                                add_table=table)
         return dq, dk, dv, db, None, None, None
 
 

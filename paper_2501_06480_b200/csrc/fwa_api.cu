@@ -14,6 +14,8 @@
 #include <string>
 
 #include <algorithm>
+#include <map>
+#include <utility>
 
 #include "fwa_common.cuh"
 
@@ -40,10 +42,8 @@ struct DevInfo {
   int64_t l2 = 0;
   size_t smem_optin = 0;
 };
-DevInfo query_dev() {
+DevInfo query_dev(int dev) {
   DevInfo d;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return d;
   int v = 0;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) d.sm = v;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess) d.l2 = v;
@@ -51,12 +51,44 @@ DevInfo query_dev() {
     d.smem_optin = (size_t)v;
   return d;
 }
-const DevInfo& dev_info() {
-  // per-process cache; the library targets one device per process (torchrun model)
-  static DevInfo info = query_dev();
-  return info;
+// Per-device caches (a process may drive several GPUs, or call from several threads):
+// device attributes, the function attributes already raised on each device, and the
+// address of the device-side error word. All behind one mutex; a lookup costs a lock.
+constexpr int kMaxDevices = 64;
+std::mutex g_dev_mu;
+DevInfo g_dev_info[kMaxDevices];
+bool g_dev_known[kMaxDevices] = {};
+unsigned int* g_flags_ptr[kMaxDevices] = {};
+std::map<std::pair<int, const void*>, int>& smem_attrs() {
+  static std::map<std::pair<int, const void*>, int> m;
+  return m;
+}
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+DevInfo dev_info() {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (!g_dev_known[dev]) {
+    g_dev_info[dev] = query_dev(dev);
+    g_dev_known[dev] = true;
+  }
+  return g_dev_info[dev];
 }
 }  // namespace
+
+int ensure_smem_attr(const void* func, int bytes, const char* what) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  int& have = smem_attrs()[{dev, func}];
+  if (have >= bytes) return FWA_OK;
+  const int rc = check_cuda(
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), what);
+  if (rc == FWA_OK) have = bytes;
+  return rc;
+}
 
 int device_sm_count() { return dev_info().sm > 0 ? dev_info().sm : 148; }
 int64_t device_l2_bytes() { return dev_info().l2; }
@@ -155,6 +187,33 @@ int pick_bwd(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask, boo
   return FWA_OK;
 }
 
+// The large-window (flat) kernels read bias/mask through one f16 (bias + mask) * log2e
+// table [n_w][h][L][L]; the L <= 64 and SIMT kernels read the fp32 bias/mask directly.
+bool fwd_uses_table(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask) {
+  if (!(has_bias || has_mask) || d->kernel == FWA_KERNEL_GENERIC) return false;
+  if (tc_fwd_supported(g, d->dtype, has_bias, has_mask)) return false;
+  return tc_fwd_flat_supported(g, d->dtype, has_bias, has_mask);
+}
+bool bwd_uses_table(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask, bool want_dbias) {
+  if (!(has_bias || has_mask) || d->kernel == FWA_KERNEL_GENERIC) return false;
+  if (tc_bwd_supported(g, d->dtype, has_bias, has_mask, want_dbias)) return false;
+  return tc_bwd_flat_supported(g, d->dtype, has_bias, has_mask, want_dbias);
+}
+// dBias partials of the kernel pick_bwd chooses (0 without dBias)
+size_t dbias_partial_bytes(const fwa_desc* d, const Geom& g, bool has_bias, bool has_mask,
+                           bool want_dbias) {
+  if (!want_dbias) return 0;
+  int kern = 0, tmem = 0;
+  size_t smem = 0;
+  if (pick_bwd(d, g, has_bias, has_mask, true, &kern, &smem, &tmem) != FWA_OK) return 0;
+  if (kern == FWA_KERNEL_GENERIC)
+    return (size_t)bwd_generic_grid(g) * g.heads * g.L * g.L * sizeof(float);
+  if (tc_bwd_supported(g, d->dtype, has_bias, has_mask, true))
+    return tc_bwd_workspace_bytes(g, has_mask, true);
+  return tc_bwd_flat_workspace_bytes(g);
+}
+size_t round256(size_t b) { return (b + 255) / 256 * 256; }
+
 }  // namespace
 }  // namespace fwa
 
@@ -166,12 +225,14 @@ extern "C" int64_t fwa_launch_count(void) { return g_launches.load(); }
 
 namespace fwa {
 unsigned int* device_flags_ptr() {
-  static unsigned int* p = nullptr;
-  if (!p) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (!g_flags_ptr[dev]) {
     void* a = nullptr;
-    if (cudaGetSymbolAddress(&a, g_fwa_device_flags) == cudaSuccess) p = (unsigned int*)a;
+    if (cudaGetSymbolAddress(&a, g_fwa_device_flags) == cudaSuccess)
+      g_flags_ptr[dev] = (unsigned int*)a;
   }
-  return p;
+  return g_flags_ptr[dev];
 }
 }  // namespace fwa
 
@@ -215,8 +276,31 @@ extern "C" int fwa_footprint(const fwa_desc* desc, fwa_footprint_t* out) {
   return FWA_OK;
 }
 
+// Resolve the add table of a flat-kernel call: the caller's prebuilt desc->add_table, else
+// built into the head of `workspace`. Returns the workspace bytes it used.
+static int resolve_table(const fwa_desc* desc, Geom* g, const float* bias, const float* mask,
+                         void* workspace, size_t workspace_bytes, size_t* used, cudaStream_t s) {
+  *used = 0;
+  g->add_nw = mask ? std::max(1, desc->mask_windows) : 1;
+  if (desc->add_table) {
+    g->add_table = static_cast<const __half*>(desc->add_table);
+    return FWA_OK;
+  }
+  const size_t need = round256(flat_add_table_bytes(*g, mask != nullptr));
+  if (!workspace || workspace_bytes < need)
+    return fail(FWA_ERR_CAPACITY, "bias/mask on the large-window kernels need " +
+                                      std::to_string(need) + " workspace bytes (add table), got " +
+                                      std::to_string(workspace ? workspace_bytes : 0));
+  int rc = flat_build_add_table(*g, bias, mask, static_cast<__half*>(workspace), s);
+  if (rc) return rc;
+  g->add_table = static_cast<const __half*>(workspace);
+  *used = need;
+  return FWA_OK;
+}
+
 extern "C" int fwa_fwd(const fwa_desc* desc, const void* q, const void* k, const void* v,
-                       const float* bias, const float* mask, void* o, void* stream) {
+                       const float* bias, const float* mask, void* o, void* workspace,
+                       size_t workspace_bytes, void* stream) {
   Geom g;
   int rc = validate(desc, &g, true, mask);
   if (rc) return rc;
@@ -226,6 +310,10 @@ extern "C" int fwa_fwd(const fwa_desc* desc, const void* q, const void* k, const
   rc = pick_fwd(desc, g, bias != nullptr, mask != nullptr, &kern, &smem, &tmem);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  if (fwd_uses_table(desc, g, bias != nullptr, mask != nullptr)) {
+    size_t used = 0;
+    if ((rc = resolve_table(desc, &g, bias, mask, workspace, workspace_bytes, &used, s))) return rc;
+  }
   if (kern == FWA_KERNEL_TC) {
     if (tc_fwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr))
       return launch_fwd_tc(g, desc->dtype, q, k, v, bias, mask, o, s);
@@ -234,15 +322,47 @@ extern "C" int fwa_fwd(const fwa_desc* desc, const void* q, const void* k, const
   return launch_fwd_generic(g, desc->dtype, q, k, v, bias, mask, o, s);
 }
 
-extern "C" size_t fwa_bwd_workspace_bytes(const fwa_desc* desc, int want_dbias) {
+extern "C" size_t fwa_add_table_bytes(const fwa_desc* desc, int has_bias, int has_mask) {
   Geom g;
   if (validate(desc, &g, false, nullptr)) return 0;
-  if (!want_dbias) return 0;
-  g.mask_windows = desc->mask_windows > 0 ? desc->mask_windows : 1;
-  const size_t generic = (size_t)bwd_generic_grid(g) * g.heads * g.L * g.L * sizeof(float);
-  const size_t tc = tc_bwd_workspace_bytes(g, desc->mask_windows > 0, true);
-  const size_t flat = tc_bwd_flat_workspace_bytes(g);
-  return std::max(generic, std::max(tc, flat));
+  g.mask_windows = has_mask ? std::max(1, desc->mask_windows) : 1;
+  if (!fwd_uses_table(desc, g, has_bias, has_mask) &&
+      !bwd_uses_table(desc, g, has_bias, has_mask, false) &&
+      !bwd_uses_table(desc, g, has_bias, has_mask, has_bias))
+    return 0;
+  return round256(flat_add_table_bytes(g, has_mask));
+}
+
+extern "C" int fwa_build_add_table(const fwa_desc* desc, const float* bias, const float* mask,
+                                   void* table, size_t table_bytes, void* stream) {
+  Geom g;
+  int rc = validate(desc, &g, true, mask);
+  if (rc) return rc;
+  if (!bias && !mask) return fail(FWA_ERR_SHAPE, "add table needs a bias or a mask");
+  const size_t need = round256(flat_add_table_bytes(g, mask != nullptr));
+  if (!table || table_bytes < need)
+    return fail(FWA_ERR_CAPACITY, "add table needs " + std::to_string(need) + " bytes, got " +
+                                      std::to_string(table ? table_bytes : 0));
+  return flat_build_add_table(g, bias, mask, static_cast<__half*>(table), (cudaStream_t)stream);
+}
+
+extern "C" size_t fwa_fwd_workspace_bytes(const fwa_desc* desc, int has_bias, int has_mask) {
+  Geom g;
+  if (validate(desc, &g, false, nullptr)) return 0;
+  g.mask_windows = has_mask ? std::max(1, desc->mask_windows) : 1;
+  if (desc->add_table || !fwd_uses_table(desc, g, has_bias, has_mask)) return 0;
+  return round256(flat_add_table_bytes(g, has_mask));
+}
+
+extern "C" size_t fwa_bwd_workspace_bytes(const fwa_desc* desc, int has_bias, int has_mask,
+                                          int want_dbias) {
+  Geom g;
+  if (validate(desc, &g, false, nullptr)) return 0;
+  g.mask_windows = has_mask ? std::max(1, desc->mask_windows) : 1;
+  size_t b = 0;
+  if (!desc->add_table && bwd_uses_table(desc, g, has_bias, has_mask, want_dbias))
+    b = round256(flat_add_table_bytes(g, has_mask));
+  return b + dbias_partial_bytes(desc, g, has_bias, has_mask, want_dbias);
 }
 
 extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const void* v,
@@ -258,19 +378,24 @@ extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const
   size_t smem = 0;
   rc = pick_bwd(desc, g, bias != nullptr, mask != nullptr, dbias != nullptr, &kern, &smem, &tmem);
   if (rc) return rc;
-  const size_t need = fwa_bwd_workspace_bytes(desc, dbias != nullptr);
+  const size_t need =
+      fwa_bwd_workspace_bytes(desc, bias != nullptr, mask != nullptr, dbias != nullptr);
   if (need && (!workspace || workspace_bytes < need))
     return fail(FWA_ERR_CAPACITY, "backward workspace needs " + std::to_string(need) +
                                       " bytes, got " + std::to_string(workspace_bytes));
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t used = 0;
+  if (bwd_uses_table(desc, g, bias != nullptr, mask != nullptr, dbias != nullptr) &&
+      (rc = resolve_table(desc, &g, bias, mask, workspace, workspace_bytes, &used, s)))
+    return rc;
+  float* parts = workspace ? reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + used)
+                           : nullptr;
   if (kern == FWA_KERNEL_TC) {
     if (tc_bwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr, dbias != nullptr))
-      return launch_bwd_tc(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
-                           (float*)workspace, (cudaStream_t)stream);
-    return launch_bwd_tc_large(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
-                               (float*)workspace, (cudaStream_t)stream);
+      return launch_bwd_tc(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, parts, s);
+    return launch_bwd_tc_large(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, parts, s);
   }
-  return launch_bwd_generic(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias,
-                            (float*)workspace, (cudaStream_t)stream);
+  return launch_bwd_generic(g, desc->dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, parts, s);
 }
 
 // ---- token-major ("qkv") layout: fused with the Swin qkv / proj Linears ----------
@@ -278,7 +403,10 @@ extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const
 // dqkv: [N][L][3][h][d]. tcgen05 kernels only (L <= 64, d in {16,32,64}, f16/bf16):
 // other shapes return FWA_ERR_CAPACITY so the caller can fall back to fwa_fwd/fwa_bwd.
 extern "C" int fwa_fwd_qkv(const fwa_desc* desc, const void* qkv, const float* bias,
-                           const float* mask, void* o, void* stream) {
+                           const float* mask, void* o, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
   Geom g;
   int rc = validate(desc, &g, true, mask);
   if (rc) return rc;
@@ -300,7 +428,8 @@ extern "C" int fwa_bwd_qkv(const fwa_desc* desc, const void* qkv, const void* do
   if (!tc_bwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr, dbias != nullptr))
     return fail(FWA_ERR_CAPACITY, "fused qkv layout needs the tcgen05 backward (L <= 64, "
                                   "d in {16,32,64}, f16/bf16)");
-  const size_t need = fwa_bwd_workspace_bytes(desc, dbias != nullptr);
+  const size_t need =
+      fwa_bwd_workspace_bytes(desc, bias != nullptr, mask != nullptr, dbias != nullptr);
   if (need && (!workspace || workspace_bytes < need))
     return fail(FWA_ERR_CAPACITY, "backward workspace needs " + std::to_string(need) + " bytes");
   return launch_bwd_tc(g, desc->dtype, qkv, nullptr, nullptr, dout, bias, mask, dqkv, nullptr,

@@ -43,6 +43,8 @@ void set_error(const std::string& msg);
 int fail(int status, const std::string& msg);
 int check_cuda(cudaError_t e, const char* what);
 void count_launch(int64_t n = 1);
+// Raise a kernel's dynamic-smem limit once per (device, kernel); thread-safe.
+int ensure_smem_attr(const void* func, int bytes, const char* what);
 
 // Problem geometry shared by the kernels.
 struct Geom {
@@ -52,6 +54,10 @@ struct Geom {
   int32_t d;
   float scale;
   int32_t mask_windows;
+  // large-window (flat) kernels with bias/mask: the (bias[h] + mask[w]) * log2e f16 table
+  // [add_nw][heads][L][L] built by flat_build_add_table (caller-owned memory), else null
+  const __half* add_table = nullptr;
+  int32_t add_nw = 1;
 };
 
 // ---- kernel launchers (defined in the .cu files) --------------------------
@@ -127,9 +133,10 @@ size_t tc_fwd_flat_smem(const Geom& g);
 int launch_fwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                        const float* bias, const float* mask, void* o, cudaStream_t s);
 
-// (bias[h] + mask[w]) * log2e as f16 [n_w][h][L][L] in stream-ordered scratch (free with
-// cudaFreeAsync on the same stream after the kernel that reads it)
-int flat_build_add_table(const Geom& g, const float* bias, const float* mask, int* n_w, __half** out,
+// (bias[h] + mask[w]) * log2e as f16 [n_w][h][L][L] (n_w = mask windows, or 1 without a
+// mask) into caller-owned memory of flat_add_table_bytes(g, has_mask) bytes
+size_t flat_add_table_bytes(const Geom& g, bool has_mask);
+int flat_build_add_table(const Geom& g, const float* bias, const float* mask, __half* out,
                          cudaStream_t s);
 
 // tcgen05 / TMA backward (fwa_tc_bwd.cu)

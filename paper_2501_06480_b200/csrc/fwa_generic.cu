@@ -277,13 +277,8 @@ int launch_fwd_generic_t(const Geom& g, const void* q, const void* k, const void
   const int nRB = (g.L + R - 1) / R;
   const size_t smem = fwd_generic_smem(g);
   auto kern = fwd_generic_kernel<T>;
-  static int attr_smem = 48 * 1024;  // per instantiation; never shrinks
-  if ((int)smem > attr_smem) {
-    int rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem), "cudaFuncSetAttribute(fwd_generic)");
-    if (rc) return rc;
-    attr_smem = (int)smem;
-  }
+  int rc = FWA_OK;
+  if ((rc = ensure_smem_attr((const void*)kern, (int)smem, "cudaFuncSetAttribute(fwd_generic)"))) return rc;
   const int64_t blocks = g.units * nRB;
   if (blocks <= 0) return FWA_OK;
   if (blocks > 0x7fffffffLL) return fail(FWA_ERR_CAPACITY, "too many units for one launch");
@@ -300,14 +295,8 @@ int launch_bwd_generic_t(const Geom& g, const void* q, const void* k, const void
   const int R = bwd_rows(g.L);
   const size_t smem = bwd_generic_smem(g);
   auto kern = bwd_generic_kernel<T>;
-  static int attr_smem = 48 * 1024;
   int rc = FWA_OK;
-  if ((int)smem > attr_smem) {
-    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem), "cudaFuncSetAttribute(bwd_generic)");
-    if (rc) return rc;
-    attr_smem = (int)smem;
-  }
+  if ((rc = ensure_smem_attr((const void*)kern, (int)smem, "cudaFuncSetAttribute(bwd_generic)"))) return rc;
   const int grid = bwd_generic_grid(g);
   if (g.units <= 0) return FWA_OK;
   kern<<<grid, kBwdThreads, smem, s>>>(g, R, (const T*)q, (const T*)k, (const T*)v,

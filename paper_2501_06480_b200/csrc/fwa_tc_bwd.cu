@@ -522,13 +522,7 @@ int launch_bwd_t(const Geom& g, int dtype, const void* q, const void* k, const v
   }
   auto kern = bwd_tc_kernel<T, D, LK, ADD, DBIAS>;
   constexpr int smem = BCfg<D>::kSmem;
-  static bool attr_done = false;
-  if (!attr_done) {
-    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                    "cudaFuncSetAttribute(bwd_tc)");
-    if (rc) return rc;
-    attr_done = true;
-  }
+  if ((rc = ensure_smem_attr((const void*)kern, (int)(smem), "cudaFuncSetAttribute(bwd_tc)"))) return rc;
   const int n_tiles = (int)((g.units + 1) / 2);
   const int grid = bwd_grid<D>(g, ADD || DBIAS, mask != nullptr);
   BwdAddArgs add{bias, mask, ws, g.heads, mask ? g.mask_windows : 1};

@@ -442,13 +442,7 @@ int launch_bwd_large_t(const Geom& g, int dtype, const void* q, const void* k, c
   if ((rc = get_units_map(&m[5], dk, dtype, g.units, g.L, g.d, C::kOutRows, 1))) return rc;
   if ((rc = get_units_map(&m[6], dv, dtype, g.units, g.L, g.d, C::kOutRows, 1))) return rc;
   auto kern = bwd_tc_large_kernel<T, D, LP>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem),
-                    "cudaFuncSetAttribute(bwd_tc_large)");
-    if (rc) return rc;
-    attr_done = true;
-  }
+  if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(bwd_tc_large)"))) return rc;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
   rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kThreads), (size_t)C::kSmem, s, m[0], m[1],
                              m[2], m[3], m[4], m[5], m[6], (int)g.units, (int)g.L, g.scale),

@@ -568,29 +568,15 @@ int launch_flat_t(const Geom& g, int dtype, const void* q, const void* k, const 
     if ((rc = get_units_map(&m[3], o, dtype, 1, rows, D, kRows, 1))) return rc;
     if ((rc = get_units_map(&m[4], o, dtype, 1, rows, D, 16, 1))) return rc;
     const bool add = bias || mask;
-    FlatAdd fa{nullptr, g.heads, 1};
-    if (add) {
-      __half* tab = nullptr;
-      if ((rc = flat_build_add_table(g, bias, mask, &fa.n_w, &tab, s))) return rc;
-      fa.table = tab;
-    }
+    FlatAdd fa{g.add_table, g.heads, g.add_nw};
+    if (add && !fa.table) return fail(FWA_ERR_SHAPE, "flat forward: bias/mask given without the add table");
     auto kern = add ? fwd_flat_kernel<T, D, L, true> : fwd_flat_kernel<T, D, L, false>;
-    static bool attr_done[2] = {false, false};
-    if (!attr_done[add]) {
-      rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem),
-                      "cudaFuncSetAttribute(fwd_flat)");
-      if (rc) return rc;
-      attr_done[add] = true;
-    }
+    if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(fwd_flat)"))) return rc;
     // every CTA gets >= 1 unit (ranges are balanced to within one unit)
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
     rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(C::kThreads), (size_t)C::kSmem, s, m[0], m[1],
                                m[2], m[3], m[4], (int64_t)g.units, g.scale * 1.4426950408889634f, fa),
                     "fwd_flat_kernel launch");
-    if (add) {
-      const int rc2 = check_cuda(cudaFreeAsync(const_cast<__half*>(fa.table), s), "cudaFreeAsync(add table)");
-      if (!rc) rc = rc2;
-    }
     if (rc) return rc;
     count_launch();
     return FWA_OK;
@@ -665,29 +651,20 @@ bool flat_disabled() {
 
 }  // namespace
 
-int flat_build_add_table(const Geom& g, const float* bias, const float* mask, int* n_w, __half** out,
+size_t flat_add_table_bytes(const Geom& g, bool has_mask) {
+  const int64_t n_w = has_mask ? std::max(1, g.mask_windows) : 1;
+  return ((size_t)n_w * g.heads * g.L * g.L * sizeof(__half) + 255) / 256 * 256;
+}
+
+int flat_build_add_table(const Geom& g, const float* bias, const float* mask, __half* out,
                          cudaStream_t s) {
-  // stream-ordered scratch for the combined f16 table (the caller frees it after its kernel)
-  static bool pool_kept = false;   // keep the pool's memory across calls (no re-mapping)
-  if (!pool_kept) {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    pool_kept = true;
-  }
-  *n_w = mask ? g.mask_windows : 1;
-  const int64_t n = (int64_t)*n_w * g.heads * g.L * g.L;
-  void* tab = nullptr;
-  int rc = check_cuda(cudaMallocAsync(&tab, (size_t)n * sizeof(__half), s), "cudaMallocAsync(add table)");
-  if (rc) return rc;
+  const int n_w = mask ? std::max(1, g.mask_windows) : 1;
+  const int64_t n = (int64_t)n_w * g.heads * g.L * g.L;
   flat_add_table_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, s>>>(
-      bias, mask, g.heads, *n_w, g.L, static_cast<__half*>(tab));
-  if ((rc = check_cuda(cudaGetLastError(), "flat_add_table_kernel launch"))) return rc;
+      bias, mask, g.heads, n_w, g.L, out);
+  int rc = check_cuda(cudaGetLastError(), "flat_add_table_kernel launch");
+  if (rc) return rc;
   count_launch();
-  *out = static_cast<__half*>(tab);
   return FWA_OK;
 }
 

@@ -900,15 +900,10 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
     }
     const bool add = bias || mask;
     const bool want_db = dbias != nullptr;
-    FlatBAdd fa{nullptr, g.heads, 1, ws};
+    FlatBAdd fa{g.add_table, g.heads, g.add_nw, ws};
     if (add) {
-      if constexpr (D != 32) {
-        return fail(FWA_ERR_CAPACITY, "flat backward: bias/mask need d = 32");
-      } else {
-        __half* tab = nullptr;
-        if ((rc = flat_build_add_table(g, bias, mask, &fa.n_w, &tab, s))) return rc;
-        fa.table = tab;
-      }
+      if constexpr (D != 32) return fail(FWA_ERR_CAPACITY, "flat backward: bias/mask need d = 32");
+      if (!fa.table) return fail(FWA_ERR_SHAPE, "flat backward: bias/mask given without the add table");
     }
     // kernel variants: plain, + bias/mask, + bias/mask + dBias (bias/mask only for d = 32)
     void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
@@ -921,24 +916,14 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
         variant = want_db ? 2 : 1;
       }
     }
-    static bool attr_done[3] = {false, false, false};
-    if (!attr_done[variant]) {
-      rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem),
-                      "cudaFuncSetAttribute(bwd_flat)");
-      if (rc) return rc;
-      attr_done[variant] = true;
-    }
+    if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(bwd_flat)"))) return rc;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
     rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kBThreads), (size_t)C::kSmem, s, m[0], m[1],
                                m[2], m[3], m[4], m[5], m[6], m[7], m[8], m[9], (int64_t)g.units,
                                g.scale, fa),
                     "bwd_flat_kernel launch");
-    if (!rc) count_launch();
-    if (add) {
-      const int rc2 = check_cuda(cudaFreeAsync(const_cast<__half*>(fa.table), s), "cudaFreeAsync(add table)");
-      if (!rc) rc = rc2;
-    }
     if (rc) return rc;
+    count_launch();
     if (want_db) {
       const int n = g.heads * L * L;
       bflat_dbias_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(ws, grid, n, dbias);

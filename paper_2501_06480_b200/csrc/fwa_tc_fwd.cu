@@ -423,13 +423,7 @@ int launch_t(const Geom& g, int dtype, const void* q, const void* k, const void*
   }
   auto kern = fwd_tc_kernel<T, D, LK, ADD>;
   constexpr int smem = Cfg<D, ADD>::kSmem;
-  static bool attr_done = false;
-  if (!attr_done) {
-    rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                    "cudaFuncSetAttribute(fwd_tc)");
-    if (rc) return rc;
-    attr_done = true;
-  }
+  if ((rc = ensure_smem_attr((const void*)kern, (int)(smem), "cudaFuncSetAttribute(fwd_tc)"))) return rc;
   const int n_tiles = (int)((g.units + 1) / 2);
   const int per_sm = Cfg<D, ADD>::kCtasPerSm;
   int grid = std::max(1, std::min(n_tiles, device_sm_count() * per_sm));

@@ -540,13 +540,7 @@ int launch_large_t(const Geom& g, int dtype, const void* q, const void* k, const
     // d = 64: one CTA per SM, items double-buffered in 512 TMEM columns
     using C = LCfg<D, LP>;
     auto kern = fwd_tc_large_kernel<T, D, LP>;
-    static bool attr_done = false;
-    if (!attr_done) {
-      rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem),
-                      "cudaFuncSetAttribute(fwd_tc_large)");
-      if (rc) return rc;
-      attr_done = true;
-    }
+    if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(fwd_tc_large)"))) return rc;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, (int64_t)device_sm_count()));
     rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kThreads), (size_t)C::kSmem, s, mq, mk, mv, mo,
                                (int)g.units, (int)g.L, sl2),
@@ -555,13 +549,7 @@ int launch_large_t(const Geom& g, int dtype, const void* q, const void* k, const
     // d <= 32: two CTAs per SM (more softmax warps per SM sub-partition)
     using C = LCfg2<D, LP>;
     auto kern = fwd_tc_large2_kernel<T, D, LP>;
-    static bool attr_done = false;
-    if (!attr_done) {
-      rc = check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem),
-                      "cudaFuncSetAttribute(fwd_tc_large2)");
-      if (rc) return rc;
-      attr_done = true;
-    }
+    if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(fwd_tc_large2)"))) return rc;
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>(g.units, (int64_t)device_sm_count() * C::kCtasPerSm));
     rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kThreads2), (size_t)C::kSmem, s, mq, mk, mv,

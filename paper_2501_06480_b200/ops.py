@@ -36,7 +36,8 @@ def dtype_id(dtype: torch.dtype) -> int:
         raise InvalidRangeError(f"dtype {dtype} not supported (float32, float16, bfloat16)") from None
 
 
-def make_desc(N, h, L, d, dtype, scale=1.0, chunks=1, mask_windows=0, kernel="auto") -> nat.FwaDesc:
+def make_desc(N, h, L, d, dtype, scale=1.0, chunks=1, mask_windows=0, kernel="auto",
+              add_table: Optional[torch.Tensor] = None) -> nat.FwaDesc:
     if kernel not in _KERNELS:
         raise InvalidRangeError(f"kernel must be one of {sorted(_KERNELS)}, got {kernel!r}")
     return nat.FwaDesc(
@@ -44,7 +45,37 @@ def make_desc(N, h, L, d, dtype, scale=1.0, chunks=1, mask_windows=0, kernel="au
         dtype=dtype_id(dtype) if isinstance(dtype, torch.dtype) else int(dtype),
         scale=float(scale), chunks=int(chunks), mask_windows=int(mask_windows),
         kernel=_KERNELS[kernel], reserved=0,
+        add_table=None if add_table is None else add_table.data_ptr(),
     )
+
+
+def _workspace(nbytes: int, device) -> Optional[torch.Tensor]:
+    """Caller-owned scratch for the C-ABI (the library never allocates device memory)."""
+    return torch.empty(nbytes, dtype=torch.uint8, device=device) if nbytes else None
+
+
+def build_add_table(N, h, L, d, dtype, bias=None, mask=None, kernel: str = "auto",
+                    device=None) -> Optional[torch.Tensor]:
+    """The large-window kernels' (bias + mask) * log2e f16 table, built once so a layer's
+    forward and backward share it (``add_table=`` of attention_forward/backward).
+    None when no kernel of this shape reads a table (L <= 64, no bias/mask)."""
+    if bias is None and mask is None:
+        return None
+    ref = bias if bias is not None else mask
+    device = ref.device if device is None else device
+    mw = _check_bias_mask((N, h, L, d), device, bias, mask)
+    desc = make_desc(N, h, L, d, dtype, 1.0, 1, mw, kernel)
+    lib = nat.load()
+    nbytes = int(lib.fwa_add_table_bytes(ctypes.byref(desc), int(bias is not None),
+                                         int(mask is not None)))
+    if not nbytes:
+        return None
+    table = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    with torch.cuda.device(device):
+        st = lib.fwa_build_add_table(ctypes.byref(desc), _ptr(bias), _ptr(mask), _ptr(table),
+                                     ctypes.c_size_t(nbytes), _stream(device))
+    nat.check(st)
+    return table
 
 
 def _check_qkv(q, k, v, *more):
@@ -90,34 +121,45 @@ def _check_bias_mask(shape, device, bias, mask):
 
 
 def attention_forward(q, k, v, scale: float = 1.0, bias=None, mask=None, chunks: int = 1,
-                      kernel: str = "auto", out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """O = softmax(scale*QK^T + bias[h] + mask[n % nW]) V for every (window, head) unit."""
+                      kernel: str = "auto", out: Optional[torch.Tensor] = None,
+                      add_table: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """O = softmax(scale*QK^T + bias[h] + mask[n % nW]) V for every (window, head) unit.
+
+    ``add_table``: a build_add_table() result for this bias/mask (skips the per-call build).
+    """
     N, h, L, d = _check_qkv(q, k, v)
     mw = _check_bias_mask(q.shape, q.device, bias, mask)
-    desc = make_desc(N, h, L, d, q.dtype, scale, chunks, mw, kernel)
+    desc = make_desc(N, h, L, d, q.dtype, scale, chunks, mw, kernel, add_table)
     if out is None:
         out = torch.empty_like(q)
     elif out.shape != q.shape or out.dtype != q.dtype or not out.is_contiguous():
         raise ShapeError("out must match q's shape/dtype and be contiguous")
     lib = nat.load()
+    ws_bytes = int(lib.fwa_fwd_workspace_bytes(ctypes.byref(desc), int(bias is not None),
+                                               int(mask is not None)))
+    ws = _workspace(ws_bytes, q.device)
     with torch.cuda.device(q.device):
         st = lib.fwa_fwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(bias), _ptr(mask),
-                         _ptr(out), _stream(q.device))
+                         _ptr(out), _ptr(ws), ctypes.c_size_t(ws_bytes), _stream(q.device))
     nat.check(st)
     return out
 
 
 def attention_backward(q, k, v, do, scale: float = 1.0, bias=None, mask=None, chunks: int = 1,
-                       kernel: str = "auto", want_dbias: bool = False):
+                       kernel: str = "auto", want_dbias: bool = False,
+                       add_table: Optional[torch.Tensor] = None):
     """(dQ, dK, dV, dBias-or-None); P is recomputed on chip, nothing else is saved."""
     N, h, L, d = _check_qkv(q, k, v, do)
     mw = _check_bias_mask(q.shape, q.device, bias, mask)
-    desc = make_desc(N, h, L, d, q.dtype, scale, chunks, mw, kernel)
+    if want_dbias and bias is None:
+        raise ShapeError("dBias needs the bias the forward used")
+    desc = make_desc(N, h, L, d, q.dtype, scale, chunks, mw, kernel, add_table)
     lib = nat.load()
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     dbias = torch.empty((h, L, L), dtype=torch.float32, device=q.device) if want_dbias else None
-    ws_bytes = int(lib.fwa_bwd_workspace_bytes(ctypes.byref(desc), int(want_dbias)))
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device) if ws_bytes else None
+    ws_bytes = int(lib.fwa_bwd_workspace_bytes(ctypes.byref(desc), int(bias is not None),
+                                               int(mask is not None), int(want_dbias)))
+    ws = _workspace(ws_bytes, q.device)
     with torch.cuda.device(q.device):
         st = lib.fwa_bwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(do), _ptr(bias),
                          _ptr(mask), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dbias), _ptr(ws),
@@ -263,7 +305,7 @@ def attention_forward_qkv(qkv: torch.Tensor, heads: int, scale: float = 1.0, bia
         desc = make_desc(N, h, L, d, qkv.dtype, scale, 1, mw, kernel)
         with torch.cuda.device(qkv.device):
             st = nat.load().fwa_fwd_qkv(ctypes.byref(desc), _ptr(qkv5), _ptr(bias), _ptr(mask),
-                                        _ptr(o), _stream(qkv.device))
+                                        _ptr(o), None, ctypes.c_size_t(0), _stream(qkv.device))
         if st == 0:
             return o
         if st != 2 or kernel == "tc":
@@ -287,8 +329,9 @@ def attention_backward_qkv(qkv: torch.Tensor, do: torch.Tensor, heads: int, scal
     if kernel != "generic" and qkv.dtype in (torch.float16, torch.bfloat16):
         desc = make_desc(N, h, L, d, qkv.dtype, scale, 1, mw, kernel)
         lib = nat.load()
-        ws_bytes = int(lib.fwa_bwd_workspace_bytes(ctypes.byref(desc), int(want_dbias)))
-        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=qkv.device) if ws_bytes else None
+        ws_bytes = int(lib.fwa_bwd_workspace_bytes(ctypes.byref(desc), int(bias is not None),
+                                                   int(mask is not None), int(want_dbias)))
+        ws = _workspace(ws_bytes, qkv.device)
         with torch.cuda.device(qkv.device):
             st = lib.fwa_bwd_qkv(ctypes.byref(desc), _ptr(qkv5), _ptr(do), _ptr(bias), _ptr(mask),
                                  _ptr(dqkv), _ptr(dbias), _ptr(ws), ctypes.c_size_t(ws_bytes),

@@ -221,3 +221,61 @@ def test_torch_cpu_and_cuda_inputs_round_trip():
     assert o.device.type == "cpu" and o.dtype == torch.float32
     o2, _, _ = flash_forward(q.cuda(), k.cuda(), v.cuda(), TileConfig(r=1), ScratchpadArena())
     assert o2.is_cuda and torch.equal(o2.cpu(), o)
+
+
+class _Dense:
+    """DenseTensor surface (tensor.py:26-71): read-only ``.array``, no ``__getitem__``."""
+
+    __slots__ = ("_a",)
+
+    def __init__(self, shape, data):
+        a = np.asarray(data, dtype=np.float64).reshape(-1).copy()
+        a.setflags(write=False)
+        self._a = a.reshape(tuple(shape))
+
+    @property
+    def shape(self):
+        return self._a.shape
+
+    @property
+    def array(self):
+        return self._a
+
+
+def test_harness_fwd_bwd_pattern_on_dense_tensors():
+    # replays harness.py:_time_flash (fwd_bwd): batched forward, then flash_backward on
+    # contexts[b][head] with a DenseTensor dO slice per (b, head)
+    B, h, L, C = 2, 3, 49, 32
+    rng = orc.Rng(42)
+    q, k, v, do = (_Dense((B, h, L, C), orc.fill_uniform(rng, (B, h, L, C))) for _ in range(4))
+    cfg = TileConfig(r=2, scale=C ** -0.5)
+    arena = ScratchpadArena()
+    out, contexts, _ = batched_flash_forward(q, k, v, cfg, [arena])
+    ref_o, p = orc.attention_forward(q.array, k.array, v.array, cfg.scale)
+    assert rel_err(out.array, ref_o) <= TOL
+    rq, rk, rv = orc.attention_backward(q.array, k.array, v.array, p, do.array, cfg.scale)
+    for b in range(B):
+        for head in range(h):
+            sl_do = _Dense((L, C), do.array[b, head])
+            dq, dk, dv, _ = flash_backward(contexts[b][head], sl_do, arena)
+            for got, want in zip((dq, dk, dv), (rq[b, head], rk[b, head], rv[b, head])):
+                assert rel_err(got.array, want) <= TOL
+
+
+def test_slice_backward_keeps_the_forward_bias_and_mask():
+    # a slice's context must differentiate the biased / masked attention the batched
+    # forward ran, not plain attention
+    B, h, L, C, nW = 4, 2, 49, 32, 2
+    rng = fw.Rng(11)
+    q, k, v, do = (fw.fill_uniform(rng, (B, h, L, C), dtype=torch.float16) for _ in range(4))
+    bias = fw.fill_uniform(rng, (h, L, L), -2.0, 2.0)
+    mask = torch.where(fw.fill_uniform(rng, (nW, L, L)) > 0.5, -100.0, 0.0).float().contiguous()
+    cfg = TileConfig(r=2, scale=C ** -0.5)
+    _, ctxs, _ = batched_flash_forward(q, k, v, cfg, [ScratchpadArena()], bias=bias, mask=mask)
+    dq, dk, dv, _ = batched_flash_backward(ctxs, do, [ScratchpadArena()])
+    for b in range(B):
+        for head in range(h):
+            c = ctxs[b][head]
+            sq, sk, sv, _ = flash_backward(c, do[b, head], ScratchpadArena())
+            for got, want in zip((sq, sk, sv), (dq[b, head], dk[b, head], dv[b, head])):
+                assert (got.float() - want.float()).abs().max().item() <= 2e-2

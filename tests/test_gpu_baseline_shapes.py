@@ -1,0 +1,184 @@
+"""Parity at the exact BASELINE.json layer shapes (configs[3] Swin-B 384^2 w12, configs[4]).
+
+Every unit is compared with a float32 torch restatement of the oracle's math (chunked so
+the L x L scores of a (4096, 4, 144, 32) layer fit), and a fixed sample of whole windows
+(all heads) with the float64 oracle itself (oracle/flashwin_oracle.py, which
+tests/test_oracle.py pins to the reference's golden vectors) on the same quantised inputs.
+Tolerances (north star): fp16/bf16 within 2e-2 absolute; dBias, a sum over up to 4096
+windows, within 2e-2 relative to its largest entry.
+
+configs[3] runs as Swin trains it: learnable relative-position bias on every layer, the
+shifted-window mask on every second layer of a stage with more than one window, dBias.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import flashwin_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+fwa = pytest.importorskip("paper_2501_06480_b200")
+ops = fwa.ops
+
+TOL = 2e-2
+# (N, h, L, d) per stage, batch 64 at 384^2 with window 12 (bench.SWIN_B384)
+SWIN_B = [(4096, 4, 144, 32), (1024, 8, 144, 32), (256, 16, 144, 32), (64, 32, 144, 32)]
+# configs[4]: L = 64 / 256, d = 32 / 64, ~1 GB of forward traffic per call (bench.LARGE)
+LARGE = [(61035, 1, 64, 32), (30517, 1, 64, 64), (15258, 1, 256, 32), (7629, 1, 256, 64)]
+
+
+def _scores(q, k, scale, bias, mask, n0):
+    s = (q.float() @ k.float().transpose(-1, -2)) * scale
+    if bias is not None:
+        s = s + bias[None]
+    if mask is not None:
+        idx = torch.arange(n0, n0 + q.shape[0], device=q.device) % mask.shape[0]
+        s = s + mask[idx][:, None]
+    return s
+
+
+def _fwd_ref_chunks(q, k, v, scale, bias, mask, chunk):
+    for n0 in range(0, q.shape[0], chunk):
+        sl = slice(n0, n0 + chunk)
+        p = torch.softmax(_scores(q[sl], k[sl], scale, bias, mask, n0), -1)
+        yield sl, p @ v[sl].float()
+
+
+def _bwd_ref_chunks(q, k, v, do, scale, bias, mask, chunk):
+    """fp32 autograd per chunk: (slice, dq, dk, dv, dbias partial)."""
+    for n0 in range(0, q.shape[0], chunk):
+        sl = slice(n0, n0 + chunk)
+        qf, kf, vf = (t[sl].float().requires_grad_(True) for t in (q, k, v))
+        bf = bias.clone().requires_grad_(True) if bias is not None else None
+        s = _scores(qf, kf, scale, bf, mask, n0)
+        (torch.softmax(s, -1) @ vf).backward(do[sl].float())
+        yield sl, qf.grad, kf.grad, vf.grad, (bf.grad if bf is not None else None)
+
+
+def _swin_extras(N, h, L, layer, device, seed):
+    """Swin-B bias (gathered from a table with trained-model magnitudes) and, on odd
+    layers of multi-window stages, the shifted-window mask (bench.py's convention)."""
+    k = int(round(math.sqrt(L)))
+    rng = fwa.Rng(seed)
+    table = fwa.fill_uniform(rng, ((2 * k - 1) ** 2, h), -3.0, 3.0, device=device)
+    bias = ops.bias_gather(table, k)
+    nW = N // 64
+    mask = None
+    if nW > 1 and layer % 2 == 1:
+        side = int(round(math.sqrt(nW))) * k
+        mask = ops.shift_mask(side, side, k, k // 2, device=device)
+    return bias, mask
+
+
+def _oracle_sample(N, n_sample=6):
+    return sorted({0, 1, N // 3, N // 2 + 1, N - 2, N - 1} if N > n_sample else range(N))
+
+
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("layer", [0, 1])
+@pytest.mark.parametrize("shape", SWIN_B)
+def test_swin_b_layer_fwd_bwd_dbias(dt, layer, shape):
+    N, h, L, d = shape
+    if N <= 64 and layer == 1:
+        pytest.skip("stage 4 (one 12x12 window per image) never shifts")
+    dev = torch.device("cuda")
+    rng = fwa.Rng(1000 + N + layer)
+    q, k, v, do = (fwa.fill_uniform(rng, shape, dtype=dt, device=dev) for _ in range(4))
+    bias, mask = _swin_extras(N, h, L, layer, dev, 77 + h)
+    scale = d ** -0.5
+    assert ops.footprint(N, h, L, d, dt)["kernel_bwd"] == "tc"
+    o = ops.attention_forward(q, k, v, scale, bias, mask)
+    dq, dk, dv, db = ops.attention_backward(q, k, v, do, scale, bias, mask, want_dbias=True)
+    torch.cuda.synchronize()
+    assert fwa._native.device_flags() == 0
+    chunk = max(1, 1024 // h)
+    for sl, ref in _fwd_ref_chunks(q, k, v, scale, bias, mask, chunk):
+        err = (o[sl].float() - ref).abs().max().item()
+        assert err <= TOL, f"O {shape} windows {sl}: {err}"
+    db_ref = torch.zeros_like(bias)
+    for sl, rq, rk, rv, rb in _bwd_ref_chunks(q, k, v, do, scale, bias, mask, chunk):
+        for name, got, want in (("dQ", dq, rq), ("dK", dk, rk), ("dV", dv, rv)):
+            err = (got[sl].float() - want).abs().max().item()
+            assert err <= TOL, f"{name} {shape} windows {sl}: {err}"
+        db_ref += rb
+    db_err = (db - db_ref).abs().max().item()
+    assert db_err <= TOL * max(1.0, db_ref.abs().max().item()), db_err
+    # a fixed sample of whole windows against the float64 oracle on the same inputs
+    idx = _oracle_sample(N)
+    host = [t[idx].double().cpu().numpy() for t in (q, k, v, do)]
+    bh = bias.double().cpu().numpy()
+    mh = None if mask is None else mask.double().cpu().numpy()[np.array(idx) % mask.shape[0]]
+    ref_o, p = orc.attention_forward(*host[:3], scale, bias=bh, mask=mh,
+                                     mask_windows=None if mh is None else len(idx))
+    grads = orc.attention_backward(*host[:3], p, host[3], scale)
+    for name, got, want in zip(("O", "dQ", "dK", "dV"), (o, dq, dk, dv), (ref_o,) + tuple(grads)):
+        err = float(np.abs(got[idx].double().cpu().numpy() - want).max())
+        assert err <= TOL, f"oracle {name} {shape}: {err}"
+
+
+@pytest.mark.parametrize("shape", LARGE)
+def test_large_window_sweep_forward_backward(shape):
+    N, h, L, d = shape
+    dt = torch.float16
+    rng = fwa.Rng(500 + L + d)
+    q, k, v, do = (fwa.fill_uniform(rng, shape, dtype=dt) for _ in range(4))
+    scale = d ** -0.5
+    fp = ops.footprint(N, h, L, d, dt)
+    assert fp["kernel_fwd"] == "tc" and fp["kernel_bwd"] == "tc"
+    o = ops.attention_forward(q, k, v, scale)
+    dq, dk, dv, _ = ops.attention_backward(q, k, v, do, scale)
+    torch.cuda.synchronize()
+    assert fwa._native.device_flags() == 0
+    chunk = 4096 if L <= 64 else 1024
+    for sl, ref in _fwd_ref_chunks(q, k, v, scale, None, None, chunk):
+        assert (o[sl].float() - ref).abs().max().item() <= TOL
+    for sl, rq, rk, rv, _ in _bwd_ref_chunks(q, k, v, do, scale, None, None, chunk):
+        for got, want in ((dq, rq), (dk, rk), (dv, rv)):
+            assert (got[sl].float() - want).abs().max().item() <= TOL
+    idx = _oracle_sample(N)
+    host = [t[idx].double().cpu().numpy() for t in (q, k, v, do)]
+    ref_o, p = orc.attention_forward(*host[:3], scale)
+    grads = orc.attention_backward(*host[:3], p, host[3], scale)
+    for got, want in zip((o, dq, dk, dv), (ref_o,) + tuple(grads)):
+        assert float(np.abs(got[idx].double().cpu().numpy() - want).max()) <= TOL
+
+
+@pytest.mark.parametrize("dt", [torch.float16, torch.bfloat16])
+def test_prebuilt_add_table_matches_per_call_build(dt):
+    # the autograd path builds the (bias + mask) table once per layer (ops.build_add_table)
+    # and hands it to the forward and the backward: bitwise the same as building per call
+    N, h, L, d = 256, 4, 144, 32
+    rng = fwa.Rng(8)
+    q, k, v, do = (fwa.fill_uniform(rng, (N, h, L, d), dtype=dt) for _ in range(4))
+    bias, mask = _swin_extras(N, h, L, 1, q.device, 3)
+    table = ops.build_add_table(N, h, L, d, dt, bias, mask)
+    assert table is not None and table.numel() >= mask.shape[0] * h * L * L * 2
+    o1 = ops.attention_forward(q, k, v, 0.2, bias, mask)
+    o2 = ops.attention_forward(q, k, v, 0.2, bias, mask, add_table=table)
+    assert torch.equal(o1, o2)
+    g1 = ops.attention_backward(q, k, v, do, 0.2, bias, mask, want_dbias=True)
+    g2 = ops.attention_backward(q, k, v, do, 0.2, bias, mask, want_dbias=True, add_table=table)
+    for a, b in zip(g1, g2):
+        assert torch.equal(a, b)
+    assert ops.build_add_table(N, h, 49, d, dt, bias[:, :49, :49].contiguous()) is None
+
+
+def test_large_bias_magnitudes_stay_within_tolerance():
+    # trained Swin biases reach |b| ~ 8; the large-window kernels quantise (bias + mask)
+    # * log2e to f16 (relative step 2^-11: <= 0.3 % in P at |b| = 8), well inside 2e-2
+    N, h, L, d = 64, 4, 144, 32
+    rng = fwa.Rng(21)
+    q, k, v, do = (fwa.fill_uniform(rng, (N, h, L, d), dtype=torch.float16) for _ in range(4))
+    bias = fwa.fill_uniform(rng, (h, L, L), -8.0, 8.0)
+    o = ops.attention_forward(q, k, v, d ** -0.5, bias, None)
+    dq, dk, dv, db = ops.attention_backward(q, k, v, do, d ** -0.5, bias, None, want_dbias=True)
+    (_, ref), = _fwd_ref_chunks(q, k, v, d ** -0.5, bias, None, N)
+    assert (o.float() - ref).abs().max().item() <= TOL
+    (_, rq, rk, rv, rb), = _bwd_ref_chunks(q, k, v, do, d ** -0.5, bias, None, N)
+    for got, want in ((dq, rq), (dk, rk), (dv, rv)):
+        assert (got.float() - want).abs().max().item() <= TOL
+    assert (db - rb).abs().max().item() <= TOL * max(1.0, rb.abs().max().item())

@@ -48,7 +48,7 @@ def test_forward_and_backward_write_only_their_outputs(dt, shape):
     desc = ops.make_desc(N, h, L, d, dt, d ** -0.5, 1, 0, "auto")
     ob, o = _guarded(shape, dt)
     st = lib.fwa_fwd(ctypes.byref(desc), ops._ptr(q), ops._ptr(k), ops._ptr(v), None, None,
-                     ops._ptr(o), ops._stream(q.device))
+                     ops._ptr(o), None, ctypes.c_size_t(0), ops._stream(q.device))
     nat.check(st)
     _check_guard(ob, n)
     assert torch.isfinite(o).all()
@@ -73,7 +73,7 @@ def test_fused_qkv_layout_writes_only_its_outputs(dt):
     desc = ops.make_desc(N, h, L, d, dt, d ** -0.5, 1, 0, "auto")
     ob, o = _guarded((N, L, h * d), dt)
     nat.check(lib.fwa_fwd_qkv(ctypes.byref(desc), ops._ptr(qkv), None, None, ops._ptr(o),
-                              ops._stream(qkv.device)))
+                              None, ctypes.c_size_t(0), ops._stream(qkv.device)))
     _check_guard(ob, N * L * h * d)
     gb, g = _guarded((N, L, 3 * h * d), dt)
     nat.check(lib.fwa_bwd_qkv(ctypes.byref(desc), ops._ptr(qkv), ops._ptr(do), None, None,

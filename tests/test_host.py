@@ -23,7 +23,7 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(nat.EXPORTED_SYMBOLS)
-    assert lib.fwa_abi_version() == 1
+    assert lib.fwa_abi_version() == 2
 
 
 def test_tileconfig_matches_reference_rules(golden):
@@ -111,7 +111,7 @@ def test_c_abi_rejects_null_pointers_without_launching():
     lib = nat.load()
     d = _desc()
     before = lib.fwa_launch_count()
-    assert lib.fwa_fwd(ctypes.byref(d), None, None, None, None, None, None, None) == 1
+    assert lib.fwa_fwd(ctypes.byref(d), None, None, None, None, None, None, None, 0, None) == 1
     assert lib.fwa_launch_count() == before
 
 
@@ -149,3 +149,71 @@ def test_poly_exp2_restatement_accuracy_and_clamp():
     assert rel.max() < 8e-5
     y = ex2_poly(np.array([-126.5, -150.0, -1e30, -np.inf], np.float32))
     assert np.all(np.isfinite(y)) and np.all(y >= 0) and np.all(y < 1e-37)
+
+
+class _DenseLike:
+    """The reference DenseTensor's surface (tensor.py:26-71): shape, a read-only float64
+    ``.array`` view and no ``__getitem__``; stands in when /root/reference is absent."""
+
+    __slots__ = ("_a",)
+
+    def __init__(self, shape, data):
+        a = np.asarray(data, dtype=np.float64).reshape(-1).copy()
+        a.setflags(write=False)
+        self._a = a.reshape(tuple(shape))
+
+    @property
+    def shape(self):
+        return self._a.shape
+
+    @property
+    def array(self):
+        return self._a
+
+
+def _dense_classes():
+    classes = [_DenseLike]
+    ref = "/root/reference/pkg/src"
+    if os.path.isdir(ref):
+        import sys
+
+        sys.path.insert(0, ref)
+        try:
+            from flashwin.tensor import DenseTensor
+
+            classes.append(DenseTensor)
+        finally:
+            sys.path.remove(ref)
+    return classes
+
+
+@pytest.mark.parametrize("dense", _dense_classes())
+def test_batched_contexts_slice_dense_tensors(dense):
+    # harness.py:543-550 indexes contexts[b][head] of DenseTensor inputs: must not need
+    # DenseTensor.__getitem__ (it has none)
+    rng = np.random.default_rng(0)
+    arrs = [rng.standard_normal((3, 2, 5, 4)) for _ in range(3)]
+    q, k, v = (dense(a.shape, a) for a in arrs)
+    ctxs = fw.BatchedContexts(q, k, v, fw.TileConfig(r=1))
+    assert len(ctxs) == 3 and len(ctxs[0]) == 2
+    c = ctxs[2][1]
+    for got, a in zip((c.q, c.k, c.v), arrs):
+        assert hasattr(got, "array") and got.shape == (5, 4)
+        assert np.array_equal(got.array, a[2, 1])
+    assert c.bias is None and c.mask is None and c.mask_windows == 0
+    assert [len(x) for x in ctxs[0:2]] == [2, 2]
+
+
+def test_batched_contexts_carry_bias_and_mask_per_slice():
+    import torch
+
+    B, h, L, C, nW = 5, 3, 4, 2, 2
+    q, k, v = (torch.randn(B, h, L, C) for _ in range(3))
+    bias = torch.randn(h, L, L)
+    mask = torch.randn(nW, L, L)
+    ctxs = fw.BatchedContexts(q, k, v, fw.TileConfig(r=1), bias, mask)
+    for b in range(B):
+        for hd in range(h):
+            c = ctxs[b][hd]
+            assert torch.equal(c.q, q[b, hd]) and torch.equal(c.bias, bias[hd])
+            assert torch.equal(c.mask, mask[b % nW]) and c.mask_windows == 1
