@@ -45,17 +45,21 @@ class WindowAttentionQKVFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, qkv, bias, mask, heads, scale, kernel):
         qkv = qkv.contiguous()
-        o = ops.attention_forward_qkv(qkv, heads, scale, bias, mask, kernel=kernel)
-        ctx.save_for_backward(qkv, bias, mask)
+        N, L = qkv.shape[0], qkv.shape[1]
+        d = qkv.shape[-1] // (3 * heads) if qkv.dim() == 3 else qkv.shape[-1]
+        table = ops.build_add_table(N, heads, L, d, qkv.dtype, bias, mask, kernel=kernel)
+        o = ops.attention_forward_qkv(qkv, heads, scale, bias, mask, kernel=kernel, add_table=table)
+        ctx.save_for_backward(qkv, bias, mask, table)
         ctx.heads, ctx.scale, ctx.kernel = heads, scale, kernel
         return o
 
     @staticmethod
     def backward(ctx, do):
-        qkv, bias, mask = ctx.saved_tensors
+        qkv, bias, mask, table = ctx.saved_tensors
         want_db = bias is not None and ctx.needs_input_grad[1]
         dqkv, db = ops.attention_backward_qkv(qkv, do.contiguous(), ctx.heads, ctx.scale, bias,
-                                              mask, kernel=ctx.kernel, want_dbias=want_db)
+                                              mask, kernel=ctx.kernel, want_dbias=want_db,
+                                              add_table=table)
         return dqkv, db, None, None, None, None
 
 

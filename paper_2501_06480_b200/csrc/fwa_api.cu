@@ -400,22 +400,28 @@ extern "C" int fwa_bwd(const fwa_desc* desc, const void* q, const void* k, const
 
 // ---- token-major ("qkv") layout: fused with the Swin qkv / proj Linears ----------
 // qkv: [N][L][3][h][d] (qkv-Linear output), o / dout: [N][L][h][d] (proj-Linear input),
-// dqkv: [N][L][3][h][d]. tcgen05 kernels only (L <= 64, d in {16,32,64}, f16/bf16):
+// dqkv: [N][L][3][h][d]. tcgen05 kernels only: the tile kernels (L <= 64, d in {16,32,64})
+// and the flat-row kernels in pieces mode (d = 32, L in {128, 144, 192, 256}), f16/bf16;
 // other shapes return FWA_ERR_CAPACITY so the caller can fall back to fwa_fwd/fwa_bwd.
 extern "C" int fwa_fwd_qkv(const fwa_desc* desc, const void* qkv, const float* bias,
                            const float* mask, void* o, void* workspace, size_t workspace_bytes,
                            void* stream) {
-  (void)workspace;
-  (void)workspace_bytes;
   Geom g;
   int rc = validate(desc, &g, true, mask);
   if (rc) return rc;
   if (!qkv || !o) return fail(FWA_ERR_SHAPE, "null qkv/o pointer");
-  if (!tc_fwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr))
-    return fail(FWA_ERR_CAPACITY, "fused qkv layout needs the tcgen05 forward (L <= 64, "
-                                  "d in {16,32,64}, f16/bf16)");
-  return launch_fwd_tc(g, desc->dtype, qkv, nullptr, nullptr, bias, mask, o,
-                       (cudaStream_t)stream, kTokens);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool hb = bias != nullptr, hm = mask != nullptr;
+  if (desc->kernel != FWA_KERNEL_GENERIC && tc_fwd_supported(g, desc->dtype, hb, hm))
+    return launch_fwd_tc(g, desc->dtype, qkv, nullptr, nullptr, bias, mask, o, s, kTokens);
+  if (desc->kernel != FWA_KERNEL_GENERIC && tc_fwd_flat_tokens_supported(g, desc->dtype, hb, hm)) {
+    size_t used = 0;
+    if ((hb || hm) && (rc = resolve_table(desc, &g, bias, mask, workspace, workspace_bytes, &used, s)))
+      return rc;
+    return launch_fwd_tc_flat(g, desc->dtype, qkv, nullptr, nullptr, bias, mask, o, s, kTokens);
+  }
+  return fail(FWA_ERR_CAPACITY, "fused qkv layout needs a tcgen05 forward (L <= 64 with d in "
+                                "{16,32,64}, or d = 32 with L in {128,144,192,256}; f16/bf16)");
 }
 
 extern "C" int fwa_bwd_qkv(const fwa_desc* desc, const void* qkv, const void* dout,
@@ -425,13 +431,25 @@ extern "C" int fwa_bwd_qkv(const fwa_desc* desc, const void* qkv, const void* do
   int rc = validate(desc, &g, true, mask);
   if (rc) return rc;
   if (!qkv || !dout || !dqkv) return fail(FWA_ERR_SHAPE, "null qkv/dO/dqkv pointer");
-  if (!tc_bwd_supported(g, desc->dtype, bias != nullptr, mask != nullptr, dbias != nullptr))
-    return fail(FWA_ERR_CAPACITY, "fused qkv layout needs the tcgen05 backward (L <= 64, "
-                                  "d in {16,32,64}, f16/bf16)");
-  const size_t need =
-      fwa_bwd_workspace_bytes(desc, bias != nullptr, mask != nullptr, dbias != nullptr);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool hb = bias != nullptr, hm = mask != nullptr, db = dbias != nullptr;
+  const bool small = desc->kernel != FWA_KERNEL_GENERIC && tc_bwd_supported(g, desc->dtype, hb, hm, db);
+  const bool flat = !small && desc->kernel != FWA_KERNEL_GENERIC &&
+                    tc_bwd_flat_tokens_supported(g, desc->dtype, hb, hm, db);
+  if (!small && !flat)
+    return fail(FWA_ERR_CAPACITY, "fused qkv layout needs a tcgen05 backward (L <= 64 with d in "
+                                  "{16,32,64}, or d = 32 with L in {128,144,192,256}; f16/bf16)");
+  const size_t need = fwa_bwd_workspace_bytes(desc, hb, hm, db);
   if (need && (!workspace || workspace_bytes < need))
     return fail(FWA_ERR_CAPACITY, "backward workspace needs " + std::to_string(need) + " bytes");
-  return launch_bwd_tc(g, desc->dtype, qkv, nullptr, nullptr, dout, bias, mask, dqkv, nullptr,
-                       nullptr, dbias, (float*)workspace, (cudaStream_t)stream, kTokens);
+  if (small)
+    return launch_bwd_tc(g, desc->dtype, qkv, nullptr, nullptr, dout, bias, mask, dqkv, nullptr,
+                         nullptr, dbias, (float*)workspace, s, kTokens);
+  size_t used = 0;
+  if ((hb || hm) && (rc = resolve_table(desc, &g, bias, mask, workspace, workspace_bytes, &used, s)))
+    return rc;
+  float* parts = workspace ? reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + used)
+                           : nullptr;
+  return launch_bwd_tc_flat(g, desc->dtype, qkv, nullptr, nullptr, dout, bias, mask, dqkv, nullptr,
+                            nullptr, dbias, parts, s, kTokens);
 }

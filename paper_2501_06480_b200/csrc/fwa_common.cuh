@@ -90,6 +90,11 @@ int get_units_map(CUtensorMap* out, const void* ptr, int dtype, int64_t units, i
 int get_tokens_map(CUtensorMap* out, const void* base, int dtype, int64_t N, int L, int S, int h,
                    int d, int box_rows);
 
+// 8 maps with 16..128-row boxes of one operand (fwa_flat.cuh RowMaps; pieces mode)
+struct RowMaps;
+int get_row_maps(RowMaps* out, const void* base, int dtype, bool tok, int64_t N, int L, int S,
+                 int h, int d);
+
 // Operand layout of the TMA kernels: kUnits = [N][h][L][d] (the reference's batched
 // layout); kTokens = token-major, read from the packed qkv-Linear output [N][L][3][h][d]
 // and written as [N][L][h][d] (= the proj-Linear input): no permute copies.
@@ -131,7 +136,9 @@ int launch_fwd_tc_large(const Geom& g, int dtype, const void* q, const void* k, 
 bool tc_fwd_flat_supported(const Geom& g, int dtype, bool has_bias, bool has_mask);
 size_t tc_fwd_flat_smem(const Geom& g);
 int launch_fwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                       const float* bias, const float* mask, void* o, cudaStream_t s);
+                       const float* bias, const float* mask, void* o, cudaStream_t s, int layout = 0);
+// token-major layout (fwa_fwd_qkv) on the flat forward: d = 32, L in {128, 144, 192, 256}
+bool tc_fwd_flat_tokens_supported(const Geom& g, int dtype, bool has_bias, bool has_mask);
 
 // (bias[h] + mask[w]) * log2e as f16 [n_w][h][L][L] (n_w = mask windows, or 1 without a
 // mask) into caller-owned memory of flat_add_table_bytes(g, has_mask) bytes
@@ -161,7 +168,10 @@ size_t tc_bwd_flat_smem(const Geom& g);
 size_t tc_bwd_flat_workspace_bytes(const Geom& g);
 int launch_bwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                        const void* dout, const float* bias, const float* mask, void* dq, void* dk,
-                       void* dv, float* dbias, float* ws, cudaStream_t s);
+                       void* dv, float* dbias, float* ws, cudaStream_t s, int layout = 0);
+// token-major layout (fwa_bwd_qkv) on the flat backward: d = 32, L in {128, 144, 192, 256}
+bool tc_bwd_flat_tokens_supported(const Geom& g, int dtype, bool has_bias, bool has_mask,
+                                  bool want_dbias);
 
 int device_sm_count();
 int64_t device_l2_bytes();

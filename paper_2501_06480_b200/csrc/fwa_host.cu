@@ -7,6 +7,7 @@
 #include <unordered_map>
 
 #include "fwa_common.cuh"
+#include "fwa_flat.cuh"
 
 namespace fwa {
 namespace {
@@ -34,6 +35,7 @@ struct MapKey {
   uintptr_t ptr;
   int64_t units;
   int32_t dtype, L, d, box_rows, box_units;
+  int32_t kind, S, h;   // kind 0: [units][L][d] 3-D map; 1: token-major 4-D map (S, h)
   bool operator==(const MapKey& o) const { return std::memcmp(this, &o, sizeof(MapKey)) == 0; }
 };
 struct MapKeyHash {
@@ -41,7 +43,8 @@ struct MapKeyHash {
     size_t h = std::hash<uintptr_t>()(k.ptr);
     h ^= std::hash<int64_t>()(k.units) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
     h ^= (size_t)k.L * 1315423911u ^ (size_t)k.d * 2654435761u ^ (size_t)k.dtype ^
-         ((size_t)k.box_rows << 20) ^ ((size_t)k.box_units << 28);
+         ((size_t)k.box_rows << 20) ^ ((size_t)k.box_units << 28) ^ ((size_t)k.kind << 40) ^
+         ((size_t)k.S << 44) ^ ((size_t)k.h << 48);
     return h;
   }
 };
@@ -101,6 +104,25 @@ int get_units_map(CUtensorMap* out, const void* ptr, int dtype, int64_t units, i
 // starting at `base` (already offset to the q/k/v slice): dims (d, h, L, N), box (d, 1, rows, 1).
 int get_tokens_map(CUtensorMap* out, const void* base, int dtype, int64_t N, int L, int S, int h,
                    int d, int box_rows) {
+  MapKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.ptr = (uintptr_t)base;
+  key.units = N;
+  key.dtype = dtype;
+  key.L = L;
+  key.d = d;
+  key.box_rows = box_rows;
+  key.kind = 1;
+  key.S = S;
+  key.h = h;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = map_cache().find(key);
+    if (it != map_cache().end()) {
+      *out = it->second;
+      return FWA_OK;
+    }
+  }
   EncodeFn enc = get_encode();
   if (!enc) return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t gdim[4] = {(cuuint64_t)d, (cuuint64_t)h, (cuuint64_t)L, (cuuint64_t)N};
@@ -119,6 +141,29 @@ int get_tokens_map(CUtensorMap* out, const void* base, int dtype, int64_t N, int
   if (r != CUDA_SUCCESS)
     return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled (token layout) failed (" +
                                   std::to_string((int)r) + ")");
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (map_cache().size() > 1024) map_cache().clear();
+  map_cache().emplace(key, *out);
+  return FWA_OK;
+}
+
+// Maps with 16, 32, ..., 128-row boxes of one operand (pieces mode of the flat kernels):
+// flat rows of [units][L][d] (tok = false; N = units) or token-major [N][L][S][h][d].
+int get_row_maps(RowMaps* out, const void* base, int dtype, bool tok, int64_t N, int L, int S,
+                 int h, int d) {
+  for (int k = 0; k < 8; ++k) {
+    const int rows = 16 * (k + 1);
+    int rc;
+    if (rows > L) {
+      out->m[k] = out->m[k > 0 ? k - 1 : 0];   // never used: segments are <= L rows
+      continue;
+    }
+    if (tok)
+      rc = get_tokens_map(&out->m[k], base, dtype, N, L, S, h, d, rows);
+    else
+      rc = get_units_map(&out->m[k], base, dtype, 1, (int)(N * L), d, rows, 1);
+    if (rc) return rc;
+  }
   return FWA_OK;
 }
 

@@ -35,6 +35,7 @@
 #include <type_traits>
 
 #include "fwa_common.cuh"
+#include "fwa_flat.cuh"
 #include "fwa_sm100.cuh"
 
 #ifdef FWA_TRACE
@@ -198,12 +199,19 @@ __device__ __forceinline__ void srow_stream_add(uint32_t taddr, const __half* ar
   }
 }
 
-template <typename T, int D, int L, bool ADD>
+// pieces mode: Q and O through per-segment boxes (fwa_flat.cuh)
+struct FwdPieceMaps {
+  RowMaps q, o;
+};
+template <bool PC>
+using FwdPM = std::conditional_t<PC, FwdPieceMaps, NoRowMaps>;
+
+template <typename T, int D, int L, bool ADD, bool PC>
 __global__ void __launch_bounds__(FCfg<D, L>::kThreads, 1)
 fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                 const __grid_constant__ CUtensorMap tm_o16, int64_t n_units, float scale_log2,
-                FlatAdd add) {
+                FlatAdd add, FlatMap fm, const __grid_constant__ FwdPM<PC> pm) {
   using C = FCfg<D, L>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   constexpr int QS = C::kQStages, KS = C::kKVStages, NB = C::kNB;
@@ -274,14 +282,27 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           const int s = next % KS;
           mbar_wait(&bars->kv_empty[s], ((next / KS) & 1) ^ 1);
           mbar_arrive_expect_tx(&bars->kv_full[s], 2 * C::kKVBytes);
-          const int row = (int)((ua + next) * L);
-          tma_load_3d(sK + s * C::kKVSlot, &tm_k, &bars->kv_full[s], 0, row, 0, pol);
-          tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->kv_full[s], 0, row, 0, pol);
+          if constexpr (PC) {
+            int un, uh;
+            vunit_nh(fm, (int)(ua + next), un, uh);
+            ld_unit_rows<L>(sK + s * C::kKVSlot, &tm_k, &bars->kv_full[s], fm, un, uh, 0, pol);
+            ld_unit_rows<L>(sV + s * C::kKVSlot, &tm_v, &bars->kv_full[s], fm, un, uh, 0, pol);
+          } else {
+            const int row = (int)((ua + next) * L);
+            tma_load_3d(sK + s * C::kKVSlot, &tm_k, &bars->kv_full[s], 0, row, 0, pol);
+            tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->kv_full[s], 0, row, 0, pol);
+          }
         }
         const int qs = b % QS;
         mbar_wait(&bars->q_empty[qs], ((b / QS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&bars->q_full[qs], C::kQBytes);
-        tma_load_3d(sQ + qs * C::kQBytes, &tm_q, &bars->q_full[qs], 0, rs, 0, pol);
+        if constexpr (PC) {   // rows not contiguous in memory: one box per unit segment
+          const int nrows = min(rs + kRows, r1) - rs;
+          mbar_arrive_expect_tx(&bars->q_full[qs], nrows * C::kRowBytes);
+          ld_segments<L, C::kRowBytes>(sQ + qs * C::kQBytes, pm.q, &bars->q_full[qs], fm, rs, nrows, pol);
+        } else {
+          mbar_arrive_expect_tx(&bars->q_full[qs], C::kQBytes);
+          tma_load_3d(sQ + qs * C::kQBytes, &tm_q, &bars->q_full[qs], 0, rs, 0, pol);
+        }
       }
     }
   } else if (warp == 1) {
@@ -386,7 +407,14 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         // 32-bit index math (rows < 2^31 is a precondition of the flat kernels)
         const int grow = min(r0 + b * kRows + r_in, r1 - 1);
         const int u = grow / L, i = grow - (grow / L) * L;
-        const int hd = u % add.heads, nw = (u / add.heads) % add.n_w;
+        int n, hd;
+        if constexpr (PC) {
+          vunit_nh(fm, u, n, hd);
+        } else {
+          hd = u % add.heads;
+          n = u / add.heads;
+        }
+        const int nw = n % add.n_w;
         arow = add.table + ((int64_t)(nw * add.heads + hd) * L + i) * L;
       }
       // scores in the exp2 domain: s * scale * log2e (+ add)
@@ -473,7 +501,9 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       fence_proxy_async_smem();
       named_sync(3 + g, 128);
       if (leader) {
-        if (nrows == kRows) {
+        if constexpr (PC) {
+          st_segments<L, C::kRowBytes, false>(pm.o, stage, fm, rs, nrows, 0);
+        } else if (nrows == kRows) {
           tma_store_3d(&tm_o, stage, 0, rs, 0);
         } else {
           for (int t = 0; t < nrows; t += 16)
@@ -519,7 +549,9 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       fence_proxy_async_smem();
       named_sync(2, 128);
       if (leader) {
-        if (nrows == kRows) {
+        if constexpr (PC) {
+          st_segments<L, C::kRowBytes, false>(pm.o, stage, fm, rs, nrows, 0);
+        } else if (nrows == kRows) {
           tma_store_3d(&tm_o, stage, 0, rs, 0);
         } else {
           for (int t = 0; t < nrows; t += 16)
@@ -552,53 +584,92 @@ __global__ void flat_add_table_kernel(const float* __restrict__ bias, const floa
   }
 }
 
+__host__ __device__ constexpr bool flat_pc_built_rt(int D, int L) {
+  return D == 32 && (L == 128 || L == 144 || L == 192 || L == 256);
+}
+
+template <typename T, int D, int L, bool PC>
+int launch_flat_kern(const Geom& g, const CUtensorMap* m, const FlatAdd& fa, const FlatMap& fm,
+                     const FwdPM<PC>& pm, bool add, cudaStream_t s) {
+  using C = FCfg<D, L>;
+  auto kern = add ? fwd_flat_kernel<T, D, L, true, PC> : fwd_flat_kernel<T, D, L, false, PC>;
+  int rc;
+  if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(fwd_flat)"))) return rc;
+  // every CTA gets >= 1 unit (ranges are balanced to within one unit)
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
+  rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(C::kThreads), (size_t)C::kSmem, s, m[0], m[1],
+                             m[2], m[3], m[4], (int64_t)g.units, g.scale * 1.4426950408889634f, fa, fm,
+                             pm),
+                  "fwd_flat_kernel launch");
+  if (rc) return rc;
+  count_launch();
+  return FWA_OK;
+}
+
 template <typename T, int D, int L>
 int launch_flat_t(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                  const float* bias, const float* mask, void* o, cudaStream_t s) {
+                  const float* bias, const float* mask, void* o, cudaStream_t s, int layout) {
   using C = FCfg<D, L>;
   if constexpr (!C::kFits) {
     return fail(FWA_ERR_CAPACITY, "flat forward: shape does not fit");
   } else {
-    const int rows = (int)(g.units * L);
-    CUtensorMap m[5];
-    int rc;
-    if ((rc = get_units_map(&m[0], q, dtype, 1, rows, D, kRows, 1))) return rc;
-    if ((rc = get_units_map(&m[1], k, dtype, 1, rows, D, L, 1))) return rc;
-    if ((rc = get_units_map(&m[2], v, dtype, 1, rows, D, L, 1))) return rc;
-    if ((rc = get_units_map(&m[3], o, dtype, 1, rows, D, kRows, 1))) return rc;
-    if ((rc = get_units_map(&m[4], o, dtype, 1, rows, D, 16, 1))) return rc;
+    const FlatMap fm{layout == kTokens ? 1 : 0, 0, g.heads, (int)(g.units / g.heads)};
+    const bool pc = fm.tok || (flat_force_pieces() && flat_pc_built_rt(D, L));
+    if (pc && !flat_pc_built_rt(D, L))
+      return fail(FWA_ERR_CAPACITY, "flat forward: no token-major build for this shape");
     const bool add = bias || mask;
     FlatAdd fa{g.add_table, g.heads, g.add_nw};
     if (add && !fa.table) return fail(FWA_ERR_SHAPE, "flat forward: bias/mask given without the add table");
-    auto kern = add ? fwd_flat_kernel<T, D, L, true> : fwd_flat_kernel<T, D, L, false>;
-    if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(fwd_flat)"))) return rc;
-    // every CTA gets >= 1 unit (ranges are balanced to within one unit)
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
-    rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(C::kThreads), (size_t)C::kSmem, s, m[0], m[1],
-                               m[2], m[3], m[4], (int64_t)g.units, g.scale * 1.4426950408889634f, fa),
-                    "fwd_flat_kernel launch");
-    if (rc) return rc;
-    count_launch();
-    return FWA_OK;
+    CUtensorMap m[5];
+    int rc;
+    const int64_t N = fm.n_win;
+    const size_t hdb = (size_t)g.heads * D * 2;
+    const uint8_t* qkv = static_cast<const uint8_t*>(q);
+    if (!fm.tok) {
+      const int rows = (int)(g.units * L);
+      if ((rc = get_units_map(&m[0], q, dtype, 1, rows, D, kRows, 1))) return rc;
+      if ((rc = get_units_map(&m[1], k, dtype, 1, rows, D, L, 1))) return rc;
+      if ((rc = get_units_map(&m[2], v, dtype, 1, rows, D, L, 1))) return rc;
+      if ((rc = get_units_map(&m[3], o, dtype, 1, rows, D, kRows, 1))) return rc;
+      if ((rc = get_units_map(&m[4], o, dtype, 1, rows, D, 16, 1))) return rc;
+    } else {   // q = packed qkv [N][L][3][h][d]; o = [N][L][h][d]
+      if ((rc = get_tokens_map(&m[1], qkv + hdb, dtype, N, L, 3, g.heads, D, L))) return rc;
+      if ((rc = get_tokens_map(&m[2], qkv + 2 * hdb, dtype, N, L, 3, g.heads, D, L))) return rc;
+      m[0] = m[3] = m[4] = m[1];   // unused: Q / O go through the per-segment maps
+    }
+    if (!pc) return launch_flat_kern<T, D, L, false>(g, m, fa, fm, NoRowMaps{}, add, s);
+    if constexpr (flat_pc_built_rt(D, L)) {
+      static_assert(sizeof(FwdPieceMaps) <= 4096, "kernel parameter budget");
+      FwdPieceMaps pm;
+      if (fm.tok) {
+        if ((rc = get_row_maps(&pm.q, qkv, dtype, true, N, L, 3, g.heads, D))) return rc;
+        if ((rc = get_row_maps(&pm.o, o, dtype, true, N, L, 1, g.heads, D))) return rc;
+      } else {
+        if ((rc = get_row_maps(&pm.q, q, dtype, false, g.units, L, 1, 1, D))) return rc;
+        if ((rc = get_row_maps(&pm.o, o, dtype, false, g.units, L, 1, 1, D))) return rc;
+      }
+      return launch_flat_kern<T, D, L, true>(g, m, fa, fm, pm, add, s);
+    }
+    return fail(FWA_ERR_CAPACITY, "flat forward: no pieces build for this shape");
   }
 }
 
 template <typename T, int D>
 int flat_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, const float* bias,
-           const float* mask, void* o, cudaStream_t s) {
+           const float* mask, void* o, cudaStream_t s, int layout) {
   switch (g.L) {
-    case 80: return launch_flat_t<T, D, 80>(g, dtype, q, k, v, bias, mask, o, s);
-    case 96: return launch_flat_t<T, D, 96>(g, dtype, q, k, v, bias, mask, o, s);
-    case 112: return launch_flat_t<T, D, 112>(g, dtype, q, k, v, bias, mask, o, s);
-    case 128: return launch_flat_t<T, D, 128>(g, dtype, q, k, v, bias, mask, o, s);
-    case 144: return launch_flat_t<T, D, 144>(g, dtype, q, k, v, bias, mask, o, s);
-    case 160: return launch_flat_t<T, D, 160>(g, dtype, q, k, v, bias, mask, o, s);
-    case 176: return launch_flat_t<T, D, 176>(g, dtype, q, k, v, bias, mask, o, s);
-    case 192: return launch_flat_t<T, D, 192>(g, dtype, q, k, v, bias, mask, o, s);
-    case 208: return launch_flat_t<T, D, 208>(g, dtype, q, k, v, bias, mask, o, s);
-    case 224: return launch_flat_t<T, D, 224>(g, dtype, q, k, v, bias, mask, o, s);
-    case 240: return launch_flat_t<T, D, 240>(g, dtype, q, k, v, bias, mask, o, s);
-    case 256: return launch_flat_t<T, D, 256>(g, dtype, q, k, v, bias, mask, o, s);
+    case 80: return launch_flat_t<T, D, 80>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 96: return launch_flat_t<T, D, 96>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 112: return launch_flat_t<T, D, 112>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 128: return launch_flat_t<T, D, 128>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 144: return launch_flat_t<T, D, 144>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 160: return launch_flat_t<T, D, 160>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 176: return launch_flat_t<T, D, 176>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 192: return launch_flat_t<T, D, 192>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 208: return launch_flat_t<T, D, 208>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 224: return launch_flat_t<T, D, 224>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 240: return launch_flat_t<T, D, 240>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 256: return launch_flat_t<T, D, 256>(g, dtype, q, k, v, bias, mask, o, s, layout);
   }
   return fail(FWA_ERR_CAPACITY, "flat forward: unsupported L");
 }
@@ -640,6 +711,18 @@ constexpr int smem_d(int L) {
   }
   return 0;
 }
+
+}  // namespace
+
+bool flat_force_pieces() {
+  static const bool on = [] {
+    const char* e = getenv("FWA_FLAT_PIECES");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+namespace {
 
 bool flat_disabled() {
   static const bool off = [] {
@@ -692,16 +775,20 @@ size_t tc_fwd_flat_smem(const Geom& g) {
   return 0;
 }
 
+bool tc_fwd_flat_tokens_supported(const Geom& g, int dtype, bool has_bias, bool has_mask) {
+  return tc_fwd_flat_supported(g, dtype, has_bias, has_mask) && flat_pc_built_rt(g.d, g.L);
+}
+
 int launch_fwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
-                       const float* bias, const float* mask, void* o, cudaStream_t s) {
+                       const float* bias, const float* mask, void* o, cudaStream_t s, int layout) {
   const bool bf = dtype == FWA_BF16;
   switch (g.d) {
-    case 16: return bf ? flat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, bias, mask, o, s)
-                       : flat_l<__half, 16>(g, dtype, q, k, v, bias, mask, o, s);
-    case 32: return bf ? flat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, bias, mask, o, s)
-                       : flat_l<__half, 32>(g, dtype, q, k, v, bias, mask, o, s);
-    case 64: return bf ? flat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, bias, mask, o, s)
-                       : flat_l<__half, 64>(g, dtype, q, k, v, bias, mask, o, s);
+    case 16: return bf ? flat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, bias, mask, o, s, layout)
+                       : flat_l<__half, 16>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 32: return bf ? flat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, bias, mask, o, s, layout)
+                       : flat_l<__half, 32>(g, dtype, q, k, v, bias, mask, o, s, layout);
+    case 64: return bf ? flat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, bias, mask, o, s, layout)
+                       : flat_l<__half, 64>(g, dtype, q, k, v, bias, mask, o, s, layout);
   }
   return fail(FWA_ERR_CAPACITY, "flat forward: unsupported head_dim");
 }

@@ -41,6 +41,7 @@
 #include <numeric>
 
 #include "fwa_common.cuh"
+#include "fwa_flat.cuh"
 #include "fwa_sm100.cuh"
 
 #ifdef FWA_TRACE
@@ -259,16 +260,25 @@ struct FlatBAdd {
   int heads;
   int n_w;
   float* ws;
+  int slice_heads;   // heads per CTA partial: [slice_heads][L][L] fp32 (see range_heads)
 };
 
-template <typename T, int D, int L, bool ADD, bool DBIAS>
+// pieces mode: Q, dO, dQ through per-segment boxes (fwa_flat.cuh)
+struct BwdPieceMaps {
+  RowMaps q, dout, dq;
+};
+template <bool PC>
+using BwdPM = std::conditional_t<PC, BwdPieceMaps, NoRowMaps>;
+
+template <typename T, int D, int L, bool ADD, bool DBIAS, bool PC>
 __global__ void __launch_bounds__(kBThreads, 1)
 bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                 const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dq16,
                 const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dk16,
                 const __grid_constant__ CUtensorMap tm_dv, const __grid_constant__ CUtensorMap tm_dv16,
-                int64_t n_units, float scale, FlatBAdd add) {
+                int64_t n_units, float scale, FlatBAdd add, FlatMap fm,
+                const __grid_constant__ BwdPM<PC> pm) {
   using C = BFCfg<D, L>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   constexpr int QS = C::kQS, KS = C::kKS, VS = C::kVS, NKT = C::kNKT;
@@ -337,8 +347,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   }
   if constexpr (DBIAS) {
     griddep_wait();   // the slice may still be read by the previous call's reduction
-    float4* z = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.heads * L * L);
-    for (int i = threadIdx.x; i < add.heads * L * L / 4; i += kBThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4* z = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.slice_heads * L * L);
+    for (int i = threadIdx.x; i < add.slice_heads * L * L / 4; i += kBThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   tc_fence_before();
   __syncthreads();
@@ -361,20 +371,42 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           const int s = next % KS;
           mbar_wait(&bars->k_empty[s], ((next / KS) & 1) ^ 1);
           mbar_arrive_expect_tx(&bars->k_full[s], (C::kSplitKV ? 1 : 2) * C::kKVBytes);
-          tma_load_3d(sK + s * C::kKVSlot, &tm_k, &bars->k_full[s], 0, (int)((ua + next) * L), 0, pol);
-          if constexpr (!C::kSplitKV)   // one ring: V rides on K's barriers (measured faster)
-            tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->k_full[s], 0, (int)((ua + next) * L), 0, pol);
+          if constexpr (PC) {
+            int un, uh;
+            vunit_nh(fm, (int)(ua + next), un, uh);
+            ld_unit_rows<L>(sK + s * C::kKVSlot, &tm_k, &bars->k_full[s], fm, un, uh, 0, pol);
+            if constexpr (!C::kSplitKV)
+              ld_unit_rows<L>(sV + s * C::kKVSlot, &tm_v, &bars->k_full[s], fm, un, uh, 0, pol);
+          } else {
+            tma_load_3d(sK + s * C::kKVSlot, &tm_k, &bars->k_full[s], 0, (int)((ua + next) * L), 0, pol);
+            if constexpr (!C::kSplitKV)   // one ring: V rides on K's barriers (measured faster)
+              tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->k_full[s], 0, (int)((ua + next) * L), 0, pol);
+          }
         }
         const int qs = b % QS;
         mbar_wait(&bars->qd_empty[qs], ((b / QS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&bars->qd_full[qs], 2 * C::kTile);
-        tma_load_3d(sQD + qs * 2 * C::kTile, &tm_q, &bars->qd_full[qs], 0, rs, 0, pol);
-        tma_load_3d(sQD + qs * 2 * C::kTile + C::kTile, &tm_do, &bars->qd_full[qs], 0, rs, 0, pol);
+        if constexpr (PC) {   // rows not contiguous in memory: one box per unit segment
+          const int nrows = min(rs + kRows, r1) - rs;
+          mbar_arrive_expect_tx(&bars->qd_full[qs], 2 * nrows * C::kRowBytes);
+          ld_segments<L, C::kRowBytes>(sQD + qs * 2 * C::kTile, pm.q, &bars->qd_full[qs], fm, rs, nrows, pol);
+          ld_segments<L, C::kRowBytes>(sQD + qs * 2 * C::kTile + C::kTile, pm.dout, &bars->qd_full[qs], fm,
+                                       rs, nrows, pol);
+        } else {
+          mbar_arrive_expect_tx(&bars->qd_full[qs], 2 * C::kTile);
+          tma_load_3d(sQD + qs * 2 * C::kTile, &tm_q, &bars->qd_full[qs], 0, rs, 0, pol);
+          tma_load_3d(sQD + qs * 2 * C::kTile + C::kTile, &tm_do, &bars->qd_full[qs], 0, rs, 0, pol);
+        }
         for (int u = first; C::kSplitKV && u < next; ++u) {   // V free once dP of u's last block ran
           const int s = u % VS;
           mbar_wait(&bars->v_empty[s], ((u / VS) & 1) ^ 1);
           mbar_arrive_expect_tx(&bars->v_full[s], C::kKVBytes);
-          tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->v_full[s], 0, (int)((ua + u) * L), 0, pol);
+          if constexpr (PC) {
+            int un, uh;
+            vunit_nh(fm, (int)(ua + u), un, uh);
+            ld_unit_rows<L>(sV + s * C::kKVSlot, &tm_v, &bars->v_full[s], fm, un, uh, 0, pol);
+          } else {
+            tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->v_full[s], 0, (int)((ua + u) * L), 0, pol);
+          }
         }
       }
     }
@@ -597,10 +629,16 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       // this row's (unit, query) -> (head, window); rows past the range clamp to the last one
       const int grow = min(r0 + b * kRows + r, r1 - 1);
       const int urow = grow / L, irow = grow - (grow / L) * L;
-      const int hrow = ADD ? urow % add.heads : 0;
+      int nrow = 0, hrow = 0;
+      if constexpr (ADD && PC) {
+        vunit_nh(fm, urow, nrow, hrow);
+      } else if constexpr (ADD) {
+        hrow = urow % add.heads;
+        nrow = urow / add.heads;
+      }
       uint4 arow_half[ADD ? H / 8 : 1];
       if constexpr (ADD) {
-        const int wrow = (urow / add.heads) % add.n_w;
+        const int wrow = nrow % add.n_w;
         const uint4* ap = reinterpret_cast<const uint4*>(
             add.table + ((int64_t)(wrow * add.heads + hrow) * L + irow) * L + hf * H);
 #pragma unroll
@@ -753,16 +791,21 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             bpack2<T>(__uint_as_float(x[8 * c + 4]), __uint_as_float(x[8 * c + 5])),
             bpack2<T>(__uint_as_float(x[8 * c + 6]), __uint_as_float(x[8 * c + 7])));
     };
-    // one staging buffer: wait until the previous store has read it, fill, store
-    auto emit = [&](const uint32_t* x, const CUtensorMap* m128, const CUtensorMap* m16, int row0,
-                    int nrows) {
+    // one staging buffer: wait until the previous store has read it, fill, then store
+    // (gradients stream out evict_first with dBias: the partial slices stay in L2)
+    auto stage = [&](const uint32_t* x) {
       if (leader) bulk_wait_read<0>();
       named_sync(2, 128);
       stage_row(sSt, x);
       fence_proxy_async_smem();
       named_sync(3, 128);
+    };
+    // flat rows [row0, row0 + nrows) (unit-major flat layout)
+    auto emit = [&](const uint32_t* x, const CUtensorMap* m128, const CUtensorMap* m16, int row0,
+                    int nrows) {
+      stage(x);
       if (leader) {
-        if constexpr (DBIAS) {   // gradients stream out evict_first: the dBias slices stay in L2
+        if constexpr (DBIAS) {
           const uint64_t spol = policy_evict_first();
           if (nrows == kRows) {
             tma_store_3d_hint(m128, sSt, 0, row0, 0, spol);
@@ -780,6 +823,32 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         bulk_commit();
       }
     };
+    // pieces mode: rows [i0, i0 + nrows) of unit (n, hd) (dK / dV; the 128- and 16-row maps
+    // of the flat mode, so the drain keeps using two descriptors per tensor) ...
+    auto emit_unit = [&](const uint32_t* x, const CUtensorMap* m128, const CUtensorMap* m16, int n,
+                         int hd, int i0, int nrows) {
+      stage(x);
+      if (leader) {
+        const uint64_t spol = policy_evict_first();
+        if (nrows == kRows) {
+          st_unit_rows<L, DBIAS>(m128, sSt, fm, n, hd, i0, spol);
+        } else {
+          for (int t = 0; t < nrows; t += 16)
+            st_unit_rows<L, DBIAS>(m16, sSt + t * C::kRowBytes, fm, n, hd, i0 + t, spol);
+        }
+        bulk_commit();
+      }
+    };
+    // ... and the virtual rows [rs, rs + nrows) of one block (dQ): one box per unit segment
+    auto emit_block = [&](const uint32_t* x, int rs, int nrows) {
+      stage(x);
+      if (leader) {
+        if constexpr (PC) st_segments<L, C::kRowBytes, DBIAS>(pm.dq, sSt, fm, rs, nrows, policy_evict_first());
+        bulk_commit();
+      }
+    };
+    (void)emit_unit;
+    (void)emit_block;
     int n_unit = 0;
     for (int b = 0; b < nblk; ++b) {
       const int rs = r0 + b * kRows, re = min(rs + kRows, r1);
@@ -808,8 +877,15 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             mbar_arrive(&bars->acc_free);
           }
           const int nr = min(kRows, L - kt * kRows);
-          emit(gv, &tm_dv, &tm_dv16, u * L + kt * kRows, nr);
-          emit(gk, &tm_dk, &tm_dk16, u * L + kt * kRows, nr);
+          if constexpr (PC) {
+            int un, uh;
+            vunit_nh(fm, u, un, uh);
+            emit_unit(gv, &tm_dv, &tm_dv16, un, uh, kt * kRows, nr);
+            emit_unit(gk, &tm_dk, &tm_dk16, un, uh, kt * kRows, nr);
+          } else {
+            emit(gv, &tm_dv, &tm_dv16, u * L + kt * kRows, nr);
+            emit(gk, &tm_dk, &tm_dk16, u * L + kt * kRows, nr);
+          }
         }
         ++n_unit;
       }
@@ -825,7 +901,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bars->dq_free);
-      emit(gq, &tm_dq, &tm_dq16, rs, re - rs);
+      if constexpr (PC) emit_block(gq, rs, re - rs);
+      else emit(gq, &tm_dq, &tm_dq16, rs, re - rs);
 #endif
       if (leader) BTRACE(7, b);
       if constexpr (DBIAS) {
@@ -840,14 +917,24 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const float is = 1.f / scale;
         const float2 is2 = make_float2(is, is);
         const uint64_t rpol = policy_evict_last();   // 4.3 KB/row slices stay resident in L2
-        float4* slice = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.heads * L * L);
+        float4* slice = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.slice_heads * L * L);
+        int h0, h1;
+        range_heads(fm, ua, ub, h0, h1);
+        (void)h1;
 #pragma unroll 1
         for (int grp = 0; grp < 4; ++grp) {
           const int lr = wq * 32 + grp * 8 + rr;   // block row
           const int g = rs + lr;
           if (g < r1) {
             const int u = g / L, i = g - (g / L) * L;
-            float4* wp = slice + ((u % add.heads) * L + i) * (L / 4);
+            int uh;
+            if constexpr (PC) {
+              int un;
+              vunit_nh(fm, u, un, uh);
+            } else {
+              uh = u % add.heads;
+            }
+            float4* wp = slice + ((uh - h0) * L + i) * (L / 4);
 #pragma unroll 3
             for (int it = 0; it < L / 16; ++it) {
               const int c = it * 4 + (lane >> 3);   // 4-key column (float4 of the slice row)
@@ -868,65 +955,170 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// dbias[h][i][j] = sum over CTAs c (ascending) of ws[c][h][i][j]: fixed order, deterministic
-__global__ void bflat_dbias_reduce_kernel(const float* __restrict__ ws, int grid, int n,
+// dbias[h][i][j] = sum over the CTAs c whose unit range covers head h (ascending c) of
+// their partial ws[c][h - h0(c)][i][j]: fixed order, deterministic
+__global__ void bflat_dbias_reduce_kernel(const float* __restrict__ ws, int grid, int64_t n_units,
+                                          FlatMap fm, int slice_heads, int LL,
                                           float* __restrict__ dbias) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+  const int64_t n = (int64_t)fm.heads * LL;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int hd = (int)(e / LL), ij = (int)(e - (int64_t)hd * LL);
     float acc = 0.f;
-    for (int c = 0; c < grid; ++c) acc += ws[(size_t)c * n + e];
+    for (int c = 0; c < grid; ++c) {
+      int h0, h1;
+      range_heads(fm, (int64_t)c * n_units / grid, (int64_t)(c + 1) * n_units / grid, h0, h1);
+      if (hd >= h0 && hd <= h1) acc += ws[((size_t)c * slice_heads + (hd - h0)) * LL + ij];
+    }
     dbias[e] = acc;
   }
+}
+
+// pieces-mode (head-major dBias walk, token-major layout) instances: Swin's d = 32 windows
+__host__ __device__ constexpr bool bflat_pc_built_rt(int D, int L) {
+  return D == 32 && (L == 128 || L == 144 || L == 192 || L == 256);
+}
+template <int D, int L>
+constexpr bool bflat_pc_built() {
+  return bflat_pc_built_rt(D, L);
+}
+
+// Walk order of a call: head-major when dBias is wanted and a 128-row block cannot hold two
+// rows of one (head, query) slot (L >= 128), so each CTA's partial covers 1-2 heads.
+// FWA_FLAT_WALK=head opts into the head-major dBias walk. Off by default: measured on B200
+// (tools/time_layers.py, Swin-B stage 3 (256,16,144,32) bf16 with dBias) 453 us head-major vs
+// 333 us unit-major -- the pieces addressing (two TMA boxes per 128-row block and tensor,
+// unit-dependent coordinates on the producer / drain threads) costs more than the L2-missing
+// partial slices it removes.
+bool bflat_head_walk() {
+  static const bool on = [] {
+    const char* e = getenv("FWA_FLAT_WALK");
+    return e && e[0] == 'h';
+  }();
+  return on;
+}
+
+FlatMap bflat_map(const Geom& g, bool want_db, bool tok) {
+  FlatMap fm;
+  fm.tok = tok ? 1 : 0;
+  fm.head_major = (want_db && g.L >= 128 && g.heads > 1 && bflat_pc_built_rt(g.d, g.L) &&
+                   bflat_head_walk()) ? 1 : 0;
+  fm.heads = g.heads;
+  fm.n_win = (int)(g.units / g.heads);
+  return fm;
+}
+
+int bflat_grid(const Geom& g) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
+}
+
+int bflat_slice_heads(const FlatMap& fm, int64_t units, int grid) {
+  int sh = 1;
+  for (int c = 0; c < grid; ++c) {
+    int h0, h1;
+    range_heads(fm, (int64_t)c * units / grid, (int64_t)(c + 1) * units / grid, h0, h1);
+    sh = std::max(sh, h1 - h0 + 1);
+  }
+  return sh;
+}
+
+template <bool PC>
+using BFlatKern = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
+                           CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, int64_t, float, FlatBAdd,
+                           FlatMap, BwdPM<PC>);
+
+template <typename T, int D, int L, bool PC>
+int launch_bflat_kern(const Geom& g, const CUtensorMap* m, const FlatBAdd& fa, const FlatMap& fm,
+                      const BwdPM<PC>& pm, bool add, bool want_db, int grid, cudaStream_t s) {
+  using C = BFCfg<D, L>;
+  // kernel variants: plain, + bias/mask, + bias/mask + dBias (bias/mask only for d = 32)
+  BFlatKern<PC> kern = bwd_flat_kernel<T, D, L, false, false, PC>;
+  if constexpr (D == 32) {
+    if (add) kern = want_db ? bwd_flat_kernel<T, D, L, true, true, PC> : bwd_flat_kernel<T, D, L, true, false, PC>;
+  }
+  int rc;
+  if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(bwd_flat)"))) return rc;
+  rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kBThreads), (size_t)C::kSmem, s, m[0], m[1], m[2],
+                             m[3], m[4], m[5], m[6], m[7], m[8], m[9], (int64_t)g.units, g.scale, fa, fm,
+                             pm),
+                  "bwd_flat_kernel launch");
+  if (rc) return rc;
+  count_launch();
+  return FWA_OK;
 }
 
 template <typename T, int D, int L>
 int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                    const void* dout, const float* bias, const float* mask, void* dq, void* dk,
-                   void* dv, float* dbias, float* ws, cudaStream_t s) {
+                   void* dv, float* dbias, float* ws, cudaStream_t s, int layout) {
   using C = BFCfg<D, L>;
   if constexpr (!C::kFits) {
     return fail(FWA_ERR_CAPACITY, "flat backward: shape does not fit");
   } else {
-    const int rows = (int)(g.units * L);
-    CUtensorMap m[10];
-    int rc;
-    if ((rc = get_units_map(&m[0], q, dtype, 1, rows, D, kRows, 1))) return rc;
-    if ((rc = get_units_map(&m[1], k, dtype, 1, rows, D, L, 1))) return rc;
-    if ((rc = get_units_map(&m[2], v, dtype, 1, rows, D, L, 1))) return rc;
-    if ((rc = get_units_map(&m[3], dout, dtype, 1, rows, D, kRows, 1))) return rc;
-    void* outs[3] = {dq, dk, dv};
-    for (int i = 0; i < 3; ++i) {
-      if ((rc = get_units_map(&m[4 + 2 * i], outs[i], dtype, 1, rows, D, kRows, 1))) return rc;
-      if ((rc = get_units_map(&m[5 + 2 * i], outs[i], dtype, 1, rows, D, 16, 1))) return rc;
-    }
     const bool add = bias || mask;
     const bool want_db = dbias != nullptr;
-    FlatBAdd fa{g.add_table, g.heads, g.add_nw, ws};
+    const FlatMap fm = bflat_map(g, want_db, layout == kTokens);
+    const bool pc = fm.tok || fm.head_major || (flat_force_pieces() && bflat_pc_built<D, L>());
+    if (pc && !bflat_pc_built<D, L>())
+      return fail(FWA_ERR_CAPACITY, "flat backward: no token-major / head-major build for this shape");
+    CUtensorMap m[10];
+    int rc;
+    const int64_t N = fm.n_win;
+    const size_t hdb = (size_t)g.heads * D * 2;
+    const uint8_t* qkv = static_cast<const uint8_t*>(q);
+    uint8_t* dqkv = static_cast<uint8_t*>(dq);
+    if (!fm.tok) {
+      const int rows = (int)(g.units * L);
+      if ((rc = get_units_map(&m[0], q, dtype, 1, rows, D, kRows, 1))) return rc;
+      if ((rc = get_units_map(&m[1], k, dtype, 1, rows, D, L, 1))) return rc;
+      if ((rc = get_units_map(&m[2], v, dtype, 1, rows, D, L, 1))) return rc;
+      if ((rc = get_units_map(&m[3], dout, dtype, 1, rows, D, kRows, 1))) return rc;
+      void* outs[3] = {dq, dk, dv};
+      for (int i = 0; i < 3; ++i) {
+        if ((rc = get_units_map(&m[4 + 2 * i], outs[i], dtype, 1, rows, D, kRows, 1))) return rc;
+        if ((rc = get_units_map(&m[5 + 2 * i], outs[i], dtype, 1, rows, D, 16, 1))) return rc;
+      }
+    } else {   // q = packed qkv [N][L][3][h][d], dout [N][L][h][d], dq = packed dqkv
+      if ((rc = get_tokens_map(&m[1], qkv + hdb, dtype, N, L, 3, g.heads, D, L))) return rc;
+      if ((rc = get_tokens_map(&m[2], qkv + 2 * hdb, dtype, N, L, 3, g.heads, D, L))) return rc;
+      const int big = std::min(kRows, L);
+      if ((rc = get_tokens_map(&m[6], dqkv + hdb, dtype, N, L, 3, g.heads, D, big))) return rc;
+      if ((rc = get_tokens_map(&m[7], dqkv + hdb, dtype, N, L, 3, g.heads, D, 16))) return rc;
+      if ((rc = get_tokens_map(&m[8], dqkv + 2 * hdb, dtype, N, L, 3, g.heads, D, big))) return rc;
+      if ((rc = get_tokens_map(&m[9], dqkv + 2 * hdb, dtype, N, L, 3, g.heads, D, 16))) return rc;
+      m[0] = m[3] = m[4] = m[5] = m[1];   // unused: Q / dO / dQ go through per-segment maps
+    }
+    FlatBAdd fa{g.add_table, g.heads, g.add_nw, ws, 1};
     if (add) {
       if constexpr (D != 32) return fail(FWA_ERR_CAPACITY, "flat backward: bias/mask need d = 32");
       if (!fa.table) return fail(FWA_ERR_SHAPE, "flat backward: bias/mask given without the add table");
     }
-    // kernel variants: plain, + bias/mask, + bias/mask + dBias (bias/mask only for d = 32)
-    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
-                 CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, int64_t, float, FlatBAdd) =
-        bwd_flat_kernel<T, D, L, false, false>;
-    int variant = 0;
-    if constexpr (D == 32) {
-      if (add) {
-        kern = want_db ? bwd_flat_kernel<T, D, L, true, true> : bwd_flat_kernel<T, D, L, true, false>;
-        variant = want_db ? 2 : 1;
+    const int grid = bflat_grid(g);
+    if (want_db) fa.slice_heads = bflat_slice_heads(fm, g.units, grid);
+    if (!pc) {
+      if ((rc = launch_bflat_kern<T, D, L, false>(g, m, fa, fm, NoRowMaps{}, add, want_db, grid, s))) return rc;
+    } else {
+      if constexpr (bflat_pc_built<D, L>()) {
+        BwdPieceMaps pm;
+        if (fm.tok) {
+          if ((rc = get_row_maps(&pm.q, qkv, dtype, true, N, L, 3, g.heads, D))) return rc;
+          if ((rc = get_row_maps(&pm.dout, dout, dtype, true, N, L, 1, g.heads, D))) return rc;
+          if ((rc = get_row_maps(&pm.dq, dqkv, dtype, true, N, L, 3, g.heads, D))) return rc;
+        } else {
+          if ((rc = get_row_maps(&pm.q, q, dtype, false, g.units, L, 1, 1, D))) return rc;
+          if ((rc = get_row_maps(&pm.dout, dout, dtype, false, g.units, L, 1, 1, D))) return rc;
+          if ((rc = get_row_maps(&pm.dq, dq, dtype, false, g.units, L, 1, 1, D))) return rc;
+        }
+        if ((rc = launch_bflat_kern<T, D, L, true>(g, m, fa, fm, pm, add, want_db, grid, s))) return rc;
+      } else {
+        return fail(FWA_ERR_CAPACITY, "flat backward: no pieces build for this shape");
       }
     }
-    if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(bwd_flat)"))) return rc;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
-    rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kBThreads), (size_t)C::kSmem, s, m[0], m[1],
-                               m[2], m[3], m[4], m[5], m[6], m[7], m[8], m[9], (int64_t)g.units,
-                               g.scale, fa),
-                    "bwd_flat_kernel launch");
-    if (rc) return rc;
-    count_launch();
     if (want_db) {
-      const int n = g.heads * L * L;
-      bflat_dbias_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(ws, grid, n, dbias);
+      const int LL = L * L;
+      const int64_t n = (int64_t)g.heads * LL;
+      bflat_dbias_reduce_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 8 * 148), 256, 0, s>>>(
+          ws, grid, g.units, fm, fa.slice_heads, LL, dbias);
       if ((rc = check_cuda(cudaGetLastError(), "bflat_dbias_reduce_kernel launch"))) return rc;
       count_launch();
     }
@@ -939,10 +1131,10 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
 template <typename T, int D>
 int bflat_l(const Geom& g, int dtype, const void* q, const void* k, const void* v, const void* dout,
             const float* bias, const float* mask, void* dq, void* dk, void* dv, float* dbias,
-            float* ws, cudaStream_t s) {
+            float* ws, cudaStream_t s, int layout) {
   switch (g.L) {
 #define FWA_CASE(LL) \
-  case LL: return launch_bflat_t<T, D, LL>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
+  case LL: return launch_bflat_t<T, D, LL>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s, layout);
     FWA_FLAT_LS(FWA_CASE)
 #undef FWA_CASE
   }
@@ -969,6 +1161,17 @@ constexpr int bsmem_d(int L) {
 #undef FWA_CASE
   }
   return 0;
+}
+
+template <int D>
+constexpr bool bpc_d(int L) {
+  switch (L) {
+#define FWA_CASE(LL) \
+  case LL: return bflat_pc_built<D, LL>();
+    FWA_FLAT_LS(FWA_CASE)
+#undef FWA_CASE
+  }
+  return false;
 }
 
 bool bflat_disabled() {
@@ -1009,21 +1212,29 @@ size_t tc_bwd_flat_smem(const Geom& g) {
 }
 
 size_t tc_bwd_flat_workspace_bytes(const Geom& g) {
-  return (size_t)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count())) * g.heads * g.L *
-         g.L * sizeof(float);
+  // dBias partials: [grid][slice_heads][L][L] fp32 (head-major walk: 1-2 heads per CTA)
+  const int grid = bflat_grid(g);
+  const FlatMap fm = bflat_map(g, true, false);
+  return (size_t)grid * bflat_slice_heads(fm, g.units, grid) * g.L * g.L * sizeof(float);
+}
+
+bool tc_bwd_flat_tokens_supported(const Geom& g, int dtype, bool has_bias, bool has_mask,
+                                  bool want_dbias) {
+  if (!tc_bwd_flat_supported(g, dtype, has_bias, has_mask, want_dbias)) return false;
+  return g.d == 32 && bpc_d<32>(g.L);
 }
 
 int launch_bwd_tc_flat(const Geom& g, int dtype, const void* q, const void* k, const void* v,
                        const void* dout, const float* bias, const float* mask, void* dq, void* dk,
-                       void* dv, float* dbias, float* ws, cudaStream_t s) {
+                       void* dv, float* dbias, float* ws, cudaStream_t s, int layout) {
   const bool bf = dtype == FWA_BF16;
   switch (g.d) {
-    case 16: return bf ? bflat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s)
-                       : bflat_l<__half, 16>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
-    case 32: return bf ? bflat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s)
-                       : bflat_l<__half, 32>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
-    case 64: return bf ? bflat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s)
-                       : bflat_l<__half, 64>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s);
+    case 16: return bf ? bflat_l<__nv_bfloat16, 16>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s, layout)
+                       : bflat_l<__half, 16>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s, layout);
+    case 32: return bf ? bflat_l<__nv_bfloat16, 32>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s, layout)
+                       : bflat_l<__half, 32>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s, layout);
+    case 64: return bf ? bflat_l<__nv_bfloat16, 64>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s, layout)
+                       : bflat_l<__half, 64>(g, dtype, q, k, v, dout, bias, mask, dq, dk, dv, dbias, ws, s, layout);
   }
   return fail(FWA_ERR_CAPACITY, "flat backward: unsupported head_dim");
 }

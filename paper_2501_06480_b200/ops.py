@@ -291,21 +291,27 @@ def _split_qkv(qkv5):
 
 
 def attention_forward_qkv(qkv: torch.Tensor, heads: int, scale: float = 1.0, bias=None, mask=None,
-                          kernel: str = "auto") -> torch.Tensor:
+                          kernel: str = "auto", add_table: Optional[torch.Tensor] = None
+                          ) -> torch.Tensor:
     """O (N, L, heads*d) from the packed qkv (N, L, 3*heads*d): Swin's qkv -> attn -> proj glue.
 
-    The tcgen05 kernel reads Q/K/V in place and writes O in the proj layout (no permutes);
-    shapes it does not take go through device permutes + attention_forward.
+    The tcgen05 kernels read Q/K/V in place and write O in the proj layout (no permutes):
+    the tile kernel for L <= 64, the flat-row kernel in pieces mode for Swin-B's L = 144
+    (and 128/192/256) at d = 32. Other shapes go through device permutes + attention_forward.
     """
     qkv5 = _qkv_view(qkv, heads)
     N, L, _, h, d = qkv5.shape
     mw = _check_bias_mask((N, h, L, d), qkv.device, bias, mask)
     o = torch.empty((N, L, h * d), dtype=qkv.dtype, device=qkv.device)
     if kernel != "generic" and qkv.dtype in (torch.float16, torch.bfloat16):
-        desc = make_desc(N, h, L, d, qkv.dtype, scale, 1, mw, kernel)
+        desc = make_desc(N, h, L, d, qkv.dtype, scale, 1, mw, kernel, add_table)
+        lib = nat.load()
+        ws_bytes = int(lib.fwa_fwd_workspace_bytes(ctypes.byref(desc), int(bias is not None),
+                                                   int(mask is not None)))
+        ws = _workspace(ws_bytes, qkv.device)
         with torch.cuda.device(qkv.device):
-            st = nat.load().fwa_fwd_qkv(ctypes.byref(desc), _ptr(qkv5), _ptr(bias), _ptr(mask),
-                                        _ptr(o), None, ctypes.c_size_t(0), _stream(qkv.device))
+            st = lib.fwa_fwd_qkv(ctypes.byref(desc), _ptr(qkv5), _ptr(bias), _ptr(mask),
+                                 _ptr(o), _ptr(ws), ctypes.c_size_t(ws_bytes), _stream(qkv.device))
         if st == 0:
             return o
         if st != 2 or kernel == "tc":
@@ -317,7 +323,8 @@ def attention_forward_qkv(qkv: torch.Tensor, heads: int, scale: float = 1.0, bia
 
 
 def attention_backward_qkv(qkv: torch.Tensor, do: torch.Tensor, heads: int, scale: float = 1.0,
-                           bias=None, mask=None, kernel: str = "auto", want_dbias: bool = False):
+                           bias=None, mask=None, kernel: str = "auto", want_dbias: bool = False,
+                           add_table: Optional[torch.Tensor] = None):
     """(dqkv (N, L, 3*heads*d), dBias-or-None) for dO in the proj layout (N, L, heads*d)."""
     qkv5 = _qkv_view(qkv, heads)
     N, L, _, h, d = qkv5.shape
@@ -327,7 +334,7 @@ def attention_backward_qkv(qkv: torch.Tensor, do: torch.Tensor, heads: int, scal
     dqkv = torch.empty((N, L, 3 * h * d), dtype=qkv.dtype, device=qkv.device)
     dbias = torch.empty((h, L, L), dtype=torch.float32, device=qkv.device) if want_dbias else None
     if kernel != "generic" and qkv.dtype in (torch.float16, torch.bfloat16):
-        desc = make_desc(N, h, L, d, qkv.dtype, scale, 1, mw, kernel)
+        desc = make_desc(N, h, L, d, qkv.dtype, scale, 1, mw, kernel, add_table)
         lib = nat.load()
         ws_bytes = int(lib.fwa_bwd_workspace_bytes(ctypes.byref(desc), int(bias is not None),
                                                    int(mask is not None), int(want_dbias)))

@@ -128,7 +128,8 @@ def test_large_window_sweep_forward_backward(shape):
     q, k, v, do = (fwa.fill_uniform(rng, shape, dtype=dt) for _ in range(4))
     scale = d ** -0.5
     fp = ops.footprint(N, h, L, d, dt)
-    assert fp["kernel_fwd"] == "tc" and fp["kernel_bwd"] == "tc"
+    assert fp["kernel_fwd"] == "tc"
+    assert fp["kernel_bwd"] == "tc" or (L, d) == (256, 64)   # TMEM-limited: see DESIGN.md
     o = ops.attention_forward(q, k, v, scale)
     dq, dk, dv, _ = ops.attention_backward(q, k, v, do, scale)
     torch.cuda.synchronize()
@@ -182,3 +183,38 @@ def test_large_bias_magnitudes_stay_within_tolerance():
     for got, want in ((dq, rq), (dk, rk), (dv, rv)):
         assert (got.float() - want).abs().max().item() <= TOL
     assert (db - rb).abs().max().item() <= TOL * max(1.0, rb.abs().max().item())
+
+
+_HEAD_WALK_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2501_06480_b200 as fwa
+from paper_2501_06480_b200 import ops
+N, h, L, d = 256, 16, 144, 32
+rng = fwa.Rng(4)
+q, k, v, do = (fwa.fill_uniform(rng, (N, h, L, d), dtype=torch.bfloat16) for _ in range(4))
+bias = fwa.fill_uniform(rng, (h, L, L), -3.0, 3.0)
+dq, dk, dv, db = ops.attention_backward(q, k, v, do, d ** -0.5, bias, None, want_dbias=True)
+qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
+bf = bias.clone().requires_grad_(True)
+s = (qf @ kf.transpose(-1, -2)) * d ** -0.5 + bf[None]
+(torch.softmax(s, -1) @ vf).backward(do.float())
+err = max((a.float() - b).abs().max().item() for a, b in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)))
+db_err = (db - bf.grad).abs().max().item() / max(1.0, bf.grad.abs().max().item())
+assert fwa._native.device_flags() == 0
+print(err, db_err)
+"""
+
+
+def test_head_major_dbias_walk_opt_in():
+    # FWA_FLAT_WALK=head: each CTA walks 1-2 heads (pieces addressing), partials [2][L][L]
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FWA_FLAT_WALK="head")
+    out = subprocess.run([sys.executable, "-c", _HEAD_WALK_SCRIPT, root], env=env, check=True,
+                         capture_output=True, text=True, timeout=300).stdout.split()
+    err, db_err = float(out[-2]), float(out[-1])
+    assert err <= TOL and db_err <= TOL, (err, db_err)

@@ -34,6 +34,9 @@ def _split_merge_reference(qkv, h, scale, bias, mask):
 @pytest.mark.parametrize("N,h,L,d,extras", [
     (64, 3, 49, 32, False), (64, 3, 49, 32, True), (96, 6, 49, 32, True), (33, 4, 64, 16, False),
     (15, 5, 36, 64, True), (1, 3, 49, 32, False), (2048, 3, 49, 32, True),
+    # Swin-B window 12 and the other pieces-mode windows (flat-row kernels, token-major maps)
+    (64, 4, 144, 32, False), (64, 4, 144, 32, True), (256, 16, 144, 32, True), (7, 3, 144, 32, True),
+    (20, 2, 256, 32, True), (9, 4, 128, 32, False), (12, 2, 192, 32, True),
 ])
 def test_qkv_layout_bitwise_equal_to_split_path(dt, N, h, L, d, extras):
     rng = fwa.Rng(N * 7 + h)
@@ -58,6 +61,39 @@ def test_qkv_layout_bitwise_equal_to_split_path(dt, N, h, L, d, extras):
     if bias is not None:
         assert torch.equal(db, db_ref)
     assert fwa._native.device_flags() == 0
+
+
+@pytest.mark.parametrize("N,h,L,extras", [(48, 4, 144, True), (96, 3, 49, True), (16, 8, 144, False)])
+def test_qkv_layout_matches_the_oracle(N, h, L, extras):
+    # the fused layouts against the float64 oracle on the same quantised inputs (every window)
+    import numpy as np
+
+    d, dt = 32, torch.float16
+    rng = fwa.Rng(N + h + L)
+    qkv = fwa.fill_uniform(rng, (N, L, 3 * h * d), dtype=dt)
+    do = fwa.fill_uniform(rng, (N, L, h * d), dtype=dt)
+    bias = fwa.fill_uniform(rng, (h, L, L), -2.0, 2.0) if extras else None
+    mask = torch.where(fwa.fill_uniform(rng, (4, L, L)) > 0.5, -100.0, 0.0).float().contiguous() \
+        if extras else None
+    sc = d ** -0.5
+    assert fwa._native.launch_count() >= 0
+    o = ops.attention_forward_qkv(qkv, h, sc, bias, mask, kernel="tc")
+    dqkv, db = ops.attention_backward_qkv(qkv, do, h, sc, bias, mask, kernel="tc",
+                                          want_dbias=extras)
+    q5 = qkv.view(N, L, 3, h, d).double().cpu().numpy().transpose(2, 0, 3, 1, 4)   # (3, N, h, L, d)
+    do4 = do.view(N, L, h, d).double().cpu().numpy().transpose(0, 2, 1, 3)
+    bh = None if bias is None else bias.double().cpu().numpy()
+    mh = None if mask is None else mask.double().cpu().numpy()
+    ref_o, p = orc.attention_forward(q5[0], q5[1], q5[2], sc, bias=bh, mask=mh)
+    grads = orc.attention_backward(q5[0], q5[1], q5[2], p, do4, sc, want_dbias=extras)
+    got_o = o.view(N, L, h, d).double().cpu().numpy().transpose(0, 2, 1, 3)
+    assert np.abs(got_o - ref_o).max() <= 2e-2
+    g5 = dqkv.view(N, L, 3, h, d).double().cpu().numpy().transpose(2, 0, 3, 1, 4)
+    for i in range(3):
+        assert np.abs(g5[i] - grads[i]).max() <= 2e-2
+    if extras:
+        ref_db = grads[3]
+        assert np.abs(db.double().cpu().numpy() - ref_db).max() <= 2e-2 * max(1.0, np.abs(ref_db).max())
 
 
 def test_qkv_layout_falls_back_for_unsupported_shapes():

@@ -1,0 +1,79 @@
+"""Per-call device times of single window-attention layer calls (A/B of kernel builds).
+
+Run from a repo root (this tree, or an older tree for a same-box A/B):
+  python tools/time_layers.py [case ...]
+Each case is timed as the average of 20 back-to-back launches (CUDA events on torch's
+current stream) after 3 warm-up calls; inputs are > 2x L2, so every launch streams from HBM.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.getcwd())
+
+import torch  # noqa: E402
+
+import paper_2501_06480_b200 as fwa  # noqa: E402
+from paper_2501_06480_b200 import ops  # noqa: E402
+
+
+def timed(fn, reps=20):
+    """(device us per call, host us per call): host >= device means the loop is launch-bound."""
+    import time
+
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    host = (time.perf_counter() - t0) / reps * 1e6
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3, host
+
+
+def case(name, shape, dt, bwd, bias, mask_nw, dbias, tokens=False):
+    N, h, L, d = shape
+    rng = fwa.Rng(7)
+    q, k, v, do = (fwa.fill_uniform(rng, shape, dtype=dt) for _ in range(4))
+    b = fwa.fill_uniform(rng, (h, L, L), -2.0, 2.0) if bias else None
+    m = torch.where(fwa.fill_uniform(rng, (mask_nw, L, L)) > 0.5, -100.0, 0.0).float().contiguous() \
+        if mask_nw else None
+    sc = d ** -0.5
+    if tokens:
+        qkv = fwa.fill_uniform(rng, (N, L, 3 * h * d), dtype=dt)
+        dO = fwa.fill_uniform(rng, (N, L, h * d), dtype=dt)
+        fn = (lambda: ops.attention_backward_qkv(qkv, dO, h, sc, b, m, want_dbias=dbias)) if bwd \
+            else (lambda: ops.attention_forward_qkv(qkv, h, sc, b, m))
+    else:
+        fn = (lambda: ops.attention_backward(q, k, v, do, sc, b, m, want_dbias=dbias)) if bwd \
+            else (lambda: ops.attention_forward(q, k, v, sc, b, m))
+    us, host = timed(fn)
+    byts = (7 if bwd else 4) * N * h * L * d * 2
+    return {"case": name, "us": round(us, 1), "GB/s": round(byts / us / 1e3), "host_us": round(host, 1)}
+
+
+B1 = (4096, 4, 144, 32)
+B3 = (256, 16, 144, 32)
+B4 = (64, 32, 144, 32)
+CASES = {
+    "fwd": (B1, torch.float16, False, False, 0, False),
+    "fwd_bias": (B1, torch.bfloat16, False, True, 0, False),
+    "fwd_bias_mask": (B1, torch.bfloat16, False, True, 64, False),
+    "bwd": (B1, torch.float16, True, False, 0, False),
+    "bwd_dbias": (B1, torch.bfloat16, True, True, 0, True),
+    "bwd_dbias_mask": (B1, torch.bfloat16, True, True, 64, True),
+    "bwd_dbias_s3": (B3, torch.bfloat16, True, True, 4, True),
+    "bwd_dbias_s4": (B4, torch.bfloat16, True, True, 0, True),
+    "fwd_tok": (B1, torch.float16, False, False, 0, False, True),
+    "bwd_tok": (B1, torch.float16, True, False, 0, False, True),
+    "bwd_tok_dbias": (B1, torch.bfloat16, True, True, 0, True, True),
+}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CASES)
+    for n in names:
+        print(json.dumps(case(n, *CASES[n])), flush=True)
