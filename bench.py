@@ -66,6 +66,9 @@ METRIC = "window-attn windows/s + % HBM roofline"
 # measured on the default run beside the headline (configs[2], [3] plain and with training
 # extras, [4] forward and forward+backward)
 EMBEDDED = ("swin_t_fwdbwd", "swin_b_fwdbwd", "swin_b_train", "large_sweep", "large_sweep_fwdbwd")
+# (B, H, C, heads, window, shift): Swin-T 224^2 stage 1 (SW-MSA) and stage 3 (W-MSA) at B=128,
+# Swin-B 384^2 window 12 stage 1 (SW-MSA) at B=64
+BLOCKS = ((128, 56, 96, 3, 7, 3), (128, 14, 384, 12, 7, 0), (64, 96, 128, 4, 12, 6))
 
 
 def load_peaks():
@@ -138,15 +141,45 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle port of flash.py Alg. 1/2, float64) on host cores
+# CPU reference on host cores: the stock reference package (baseline/_ref, installed
+# from /root/reference/pkg) through its own public API, else the oracle port
 # ---------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def ref_kind() -> str:
+    return "reference" if os.path.isdir(os.path.join(REF_DIR, "flashwin")) else "port"
+
+
 def _cpu_worker(args):
-    layers, batch, n_images, bwd, seed = args
+    layers, batch, n_images, bwd, seed, kind = args
+    spent = 0.0
+    windows = 0
+    if kind == "reference":
+        # the reference's own code path, as its harness times it (harness.py:537-559):
+        # batched_flash_forward over the (B, h, L, C) stack, then flash_backward per slice
+        sys.path.insert(0, REF_DIR)
+        import flashwin as fw
+
+        rng = fw.Rng(seed)
+        for (N, h, L, d) in layers:
+            n = max(1, N // batch) * n_images
+            q, kk, v = (fw.fill_uniform(rng, (n, h, L, d), -1.0, 1.0) for _ in range(3))
+            do = fw.fill_uniform(rng, (n, h, L, d), -1.0, 1.0) if bwd else None
+            cfg = fw.TileConfig(r=max(1, d // 16), scale=d ** -0.5)
+            arena = fw.ScratchpadArena(1 << 20)   # L = 144 backward needs > the 128 KB default
+            t0 = time.perf_counter()  # inputs are resident before timing, like the GPU arm
+            _, ctxs, _ = fw.batched_flash_forward(q, kk, v, cfg, [arena])
+            if bwd:
+                for b in range(n):
+                    for hd in range(h):
+                        fw.flash_backward(ctxs[b][hd], fw.DenseTensor((L, d), do.array[b, hd]), arena)
+            spent += time.perf_counter() - t0
+            windows += n
+        return windows, spent
     from oracle import flashwin_oracle as orc
 
     rng = orc.Rng(seed)
-    spent = 0.0
-    windows = 0
     for (N, h, L, d) in layers:
         n = max(1, N // batch) * n_images
         q, kk, v = (orc.fill_uniform(rng, (n, h, L, d)) for _ in range(3))
@@ -162,7 +195,8 @@ def _cpu_worker(args):
 
 
 def cpu_reference(wl, seconds_target=12.0, steps=1, warmup=0):
-    """Time the oracle port on all host cores; returns (windows/s, cores, sample, s/step)."""
+    """Time the reference CPU path on all host cores (one process per core, each on its own
+    shard, inputs resident); returns (windows/s, cores, sample, s/step, kind)."""
     import multiprocessing as mp
 
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
@@ -172,23 +206,30 @@ def cpu_reference(wl, seconds_target=12.0, steps=1, warmup=0):
     # one CPU sample "image" = N / cpu_div windows of every layer (cpu_div defaults to the
     # batch: one real image; the large sweep has no images, 1/512 of each ~1 GB call)
     div = wl.get("cpu_div", wl["batch"])
-    _, t = _cpu_worker((layers, div, 1, wl["bwd"], 1))
+    kind = ref_kind()
+    _, t = _cpu_worker((layers, div, 1, wl["bwd"], 1, kind))
     per_proc = max(1, int(seconds_target / max(t, 1e-3) / max(steps + warmup, 1)))
     results = []
     # spawn, not fork: the parent holds a CUDA context (forking it can hang the children)
     with mp.get_context("spawn").Pool(cores) as pool:
         for s in range(warmup + steps):
-            outs = pool.map(_cpu_worker, [(layers, div, per_proc, wl["bwd"], 100 + i)
+            outs = pool.map(_cpu_worker, [(layers, div, per_proc, wl["bwd"], 100 + i, kind)
                                           for i in range(cores)])
             if s >= warmup:
                 results.append((sum(o[0] for o in outs), max(o[1] for o in outs)))
     windows = sum(r[0] for r in results)
     secs = sum(r[1] for r in results)
     unit = "image(s)" if div == wl["batch"] else f"1/{div}-of-call slice(s)"
+    what = ("the stock reference flashwin (baseline/_ref) batched_flash_forward"
+            + (" + per-slice flash_backward" if wl["bwd"] else "")
+            + (" (the reference has no Swin bias / mask: computed without them)"
+               if wl.get("extras") else "")
+            if kind == "reference" else
+            f"float64 oracle port of flash.py Alg.1{'/2' if wl['bwd'] else ''}")
     sample = (f"{per_proc} {unit} x {cores} processes per step through all {len(layers)} "
-              f"layers, float64 oracle port of flash.py Alg.1{'/2' if wl['bwd'] else ''} "
-              f"(numpy, 1 BLAS thread per process; windows/s = windows / slowest process time)")
-    return windows / secs, cores, sample, secs / max(len(results), 1)
+              f"layers, {what} (numpy float64, 1 BLAS thread per process; windows/s = windows / "
+              f"slowest process time)")
+    return windows / secs, cores, sample, secs / max(len(results), 1), kind
 
 
 # ---------------------------------------------------------------------------
@@ -346,6 +387,18 @@ def streamed_launch_ms(torch, work, i, fwd, bwd, reps=20):
 L2_BYTES = 126 * 1024 * 1024
 
 
+def shard_workload(wl, rank, world):
+    """Strong scaling: this rank's contiguous range of the workload's fixed global batch
+    (shard.shard_images: whole images, so window n keeps its mask index n mod nW)."""
+    from paper_2501_06480_b200.shard import shard_images
+
+    sh = shard_images(wl["batch"], 1, rank, world)
+    images = sh.images
+    out = dict(wl, batch=images,
+               layers=[((N // wl["batch"]) * images, h, L, d) for (N, h, L, d) in wl["layers"]])
+    return out, images
+
+
 def measure(args, name, dev, rank, world, dist, steps, with_e2e):
     import torch
 
@@ -353,6 +406,10 @@ def measure(args, name, dev, rank, world, dist, steps, with_e2e):
     from paper_2501_06480_b200 import _native as nat
 
     wl = WORKLOADS[name]
+    global_windows = None
+    if args.strong:
+        global_windows = sum(N for (N, h, L, d) in wl["layers"])
+        wl, _ = shard_workload(wl, rank, world)
     work = GpuWorkload(wl, dev, 42 + rank)
     ms_step, launches = timed_graph(torch, nat, work, steps, args.warmup, args.eager,
                                     args.soak_s, world, dist)
@@ -398,18 +455,19 @@ def measure(args, name, dev, rank, world, dist, steps, with_e2e):
             "how": how,
             "launches": kern,
             "step_frac": byts / (ms_step / 1e3) / 1e9 / peak}
-    out = {"value": windows * world / (ms_step / 1e3), "ms_per_step": ms_step,
+    total_windows = global_windows if global_windows is not None else windows * world
+    out = {"value": total_windows / (ms_step / 1e3), "ms_per_step": ms_step,
            "tflops": work.flops_per_step() * world / (ms_step / 1e3) / 1e12,
            "hbm_frac_step": byts / (ms_step / 1e3) / 1e9 / peak, "roofline": roof,
            "gpu_launches": launches, "algorithmic_bytes_per_step": byts}
     if with_e2e:
-        out["e2e"] = e2e(args, work, world, dist)
+        out["e2e"] = e2e(args, work, world, dist, total_windows)
     del work
     torch.cuda.empty_cache()
     return out
 
 
-def e2e(args, work, world, dist):
+def e2e(args, work, world, dist, total_windows):
     """Same metric through the public API on pinned HOST buffers (H2D + kernels + D2H)."""
     import torch
 
@@ -440,7 +498,7 @@ def e2e(args, work, world, dist):
     if world > 1:
         s = max_over_ranks(torch, dist, s, work.dev)
     per = [N * h * L * d * work.eb for (N, h, L, d) in wl["layers"]]
-    return {"value": sum(N for (N, h, L, d) in wl["layers"]) * world / s, "unit": "windows/s",
+    return {"value": total_windows / s, "unit": "windows/s",
             "h2d_bytes_per_step": (4 if wl["bwd"] else 3) * sum(per),
             "d2h_bytes_per_step": (3 if wl["bwd"] else 1) * sum(per),
             "path": "paper_2501_06480_b200.batched_flash_forward"
@@ -480,24 +538,46 @@ def run_gpu(args):
             embedded[name] = measure(args, name, dev, rank, world, dist,
                                      max(3, args.steps // 4), False)
     extra = embedded.get("swin_t_fwdbwd")
+    blocks = None
+    if args.workload == "swin_t_fwd" and not args.no_extra and world == 1:
+        # SURVEY 8(f)4 / PAPER.md:257-260: the whole (S)W-MSA block, fwd + bwd, on the package's
+        # kernels vs the same block in plain PyTorch ops (same weights, bf16, eager)
+        from paper_2501_06480_b200.swin import block_speedup
+
+        blocks = [block_speedup(*cfg) for cfg in BLOCKS]
     clocks = sampler.stop()
+    validation = None
+    if world > 1 and not args.no_validate:
+        # 1-GPU vs G-GPU bitwise check of the sharded path over the job's process group
+        # (NCCL all_gather of per-window bit hashes; outside every timed region)
+        from paper_2501_06480_b200.shard import validate_sharding
+
+        N0, h0, L0, d0 = WORKLOADS[args.workload]["layers"][0]
+        validation = validate_sharding(rank, world, dev, (N0, h0, L0, d0),
+                                       WORKLOADS[args.workload]["batch"])
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, cores, sample, _ = cpu_reference(wl, seconds_target=args.cpu_seconds)
-        cpu = {"value": v, "unit": "windows/s", "cores": cores, "kind": "port", "sample": sample}
+        v, cores, sample, _, kind = cpu_reference(wl, seconds_target=args.cpu_seconds)
+        cpu = {"value": v, "unit": "windows/s", "cores": cores, "kind": kind, "sample": sample}
     if rank == 0:
         line = {
             "metric": f"{METRIC} ({wl['desc']})", "value": main_res["value"], "unit": "windows/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": main_res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": main_res["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None,
             "dtype": {"float16": "f16", "bfloat16": "bf16"}[wl["dtype"]],
             "data": "synthetic (SplitMix64 U[-1,1), seed 42+rank; random bias table)",
             "config": {"workload": args.workload, "desc": wl["desc"],
-                       "images_per_gpu": wl["batch"], "global_batch": wl["batch"] * world,
+                       "images_per_gpu": wl["batch"] if not args.strong else
+                       f"{wl['batch'] // world}-{-(-wl['batch'] // world)} (shard of {wl['batch']})",
+                       "global_batch": wl["batch"] * (1 if args.strong else world),
                        "layers": [list(x) for x in wl["layers"]],
-                       "parallelism": f"dp{world} (weak: {wl['batch']} images per GPU, "
-                                      "no collective on the hot path)",
+                       "parallelism": f"dp{world} ("
+                                      + (f"strong: {wl['batch']} images split over the ranks"
+                                         if args.strong else
+                                         f"weak: {wl['batch']} images per GPU")
+                                      + ", no collective on the hot path)",
                        "launch": "eager" if args.eager else
                                  "one step captured in a CUDA graph, PDL between kernels",
                        "l2": f"no flush for the step: "
@@ -508,6 +588,16 @@ def run_gpu(args):
             "roofline": main_res["roofline"], "gpu_launches": main_res["gpu_launches"],
             "e2e": main_res.get("e2e"), "cpu_baseline": cpu, "clocks": clocks,
         }
+        if validation is not None:
+            line["validation"] = validation
+        if blocks is not None:
+            line["swin_block"] = {
+                "what": "Swin (S)W-MSA block forward + backward (partition + qkv Linear + window "
+                        "attention with rel-pos bias / shift mask + proj Linear + reverse), "
+                        "paper_2501_06480_b200.SwinWindowAttention vs the same block in plain "
+                        "PyTorch ops with shared weights (TorchSwinWindowAttention), bf16, eager, "
+                        "CUDA events, mean of 20 steps",
+                "configs": blocks}
         def summary(name, res):
             w = WORKLOADS[name]
             return {"workload": name, "desc": w["desc"], "value": res["value"],
@@ -531,18 +621,22 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if int(os.environ.get("RANK", "0")) != 0:
         return
-    v, cores, sample, per_step = cpu_reference(wl, seconds_target=args.cpu_seconds,
-                                               steps=args.steps, warmup=args.warmup)
+    v, cores, sample, per_step, kind = cpu_reference(wl, seconds_target=args.cpu_seconds,
+                                                     steps=args.steps, warmup=args.warmup)
     print(json.dumps({
         "impl": "reference", "metric": f"{METRIC} ({wl['desc']})", "value": v,
         "unit": "windows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64 U[-1,1))",
         "config": {"workload": args.workload, "desc": wl["desc"],
-                   "note": "reference CPU path = oracle port (oracle/flashwin_oracle.py) of "
-                           "flash.py Alg.1/2 in float64 on all host cores; the reference package "
-                           "is pure Python and is not shipped to the GPU box"},
-        "cpu_baseline": {"value": v, "unit": "windows/s", "cores": cores, "kind": "port",
+                   "note": ("reference CPU path = the unmodified reference package (flashwin "
+                            "0.1.0, pip-installed offline from /root/reference/pkg into "
+                            "baseline/_ref) through its public batched_flash_forward / "
+                            "flash_backward, float64, one process per host core"
+                            if kind == "reference" else
+                            "reference CPU path = oracle port (oracle/flashwin_oracle.py) of "
+                            "flash.py Alg.1/2 in float64 on all host cores (baseline/_ref absent)")},
+        "cpu_baseline": {"value": v, "unit": "windows/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": v, "unit": "windows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -561,6 +655,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the embedded fwd+bwd line")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the timed steps")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: split the workload's global batch over the ranks")
+    ap.add_argument("--no-validate", action="store_true",
+                    help="skip the post-timing 1-GPU vs G-GPU bitwise check (N > 1)")
     ap.add_argument("--soak-s", type=float, default=1.5, help="loaded seconds before timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # timing rule: at least 3 warm-up steps

@@ -43,6 +43,7 @@ from .errors import (
     ShapeError,
 )
 from .rng import Rng, fill_uniform
+from .swin import SwinWindowAttention, TorchSwinWindowAttention
 from .tiling import (
     DEFAULT_CAPACITY_BYTES,
     FlashContext,
@@ -75,7 +76,9 @@ __all__ = [
     "Rng",
     "ScratchpadArena",
     "ShapeError",
+    "SwinWindowAttention",
     "TileConfig",
+    "TorchSwinWindowAttention",
     "TrafficReport",
     "WindowAttentionFunction",
     "WindowAttentionQKVFunction",

@@ -57,3 +57,18 @@ def fill_uniform(rng: Rng, shape, lo: float = -1.0, hi: float = 1.0, dtype=torch
     ops.fill_uniform_(out, rng._state, lo, hi)
     rng._state = (rng._state + math.prod(shape) * GOLDEN) & MASK64
     return out
+
+
+def fill_uniform_at(state: int, offset: int, shape, lo: float = -1.0, hi: float = 1.0,
+                    dtype=torch.float32, device="cuda") -> torch.Tensor:
+    """Elements [offset, offset + prod(shape)) of the stream a fill_uniform from ``state``
+    would draw: a rank fills only its shard of a global tensor, bit-identical to the
+    corresponding slice of the whole draw (SplitMix64 is counter-based)."""
+    shape = tuple(int(e) for e in shape)
+    if not shape or any(e < 1 for e in shape):
+        raise ShapeError(f"all extents must be >= 1, got {shape}")
+    if not (math.isfinite(lo) and math.isfinite(hi)) or lo >= hi:
+        raise InvalidRangeError(f"need lo < hi, got lo={lo}, hi={hi}")
+    out = torch.empty(shape, dtype=dtype, device=device)
+    ops.fill_uniform_(out, (int(state) + int(offset) * GOLDEN) & MASK64, lo, hi)
+    return out

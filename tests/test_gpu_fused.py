@@ -195,3 +195,27 @@ def test_swin_b_block_window12_matches_torch(shift):
     assert (y - y_ref).abs().max().item() <= 3e-2 * y_ref.abs().max().item()
     for got, want in zip((x.grad, qkv_lin.weight.grad, proj.weight.grad, table.grad), grads_ref):
         assert (got - want).abs().max().item() <= 3e-2 * max(1e-3, want.abs().max().item())
+
+
+@pytest.mark.parametrize("B,H,C,heads,k,shift", [(4, 28, 96, 3, 7, 3), (2, 24, 128, 4, 12, 6),
+                                                 (2, 14, 384, 12, 7, 0)])
+def test_swin_block_module_matches_torch_block(B, H, C, heads, k, shift):
+    # fwa.SwinWindowAttention (kernels end to end) vs TorchSwinWindowAttention (plain torch
+    # ops, same weights), bf16, forward and backward
+    torch.manual_seed(1)
+    blk = fwa.SwinWindowAttention(C, heads, k, shift)
+    ref = fwa.TorchSwinWindowAttention(blk)
+    x = torch.randn(B, H, H, C, device="cuda", dtype=torch.bfloat16)
+    g = torch.randn_like(x)
+    outs = []
+    for m in (blk, ref):
+        xr = x.clone().requires_grad_(True)
+        y = m(xr)
+        y.backward(g)
+        outs.append((y.float(), xr.grad.float(), blk.qkv.weight.grad.float().clone(),
+                     blk.table.grad.float().clone()))
+        for t in (blk.qkv.weight, blk.qkv.bias, blk.proj.weight, blk.proj.bias, blk.table):
+            t.grad = None
+    for a, b in zip(*outs):
+        tol = 3e-2 * max(1.0, b.abs().max().item())
+        assert (a - b).abs().max().item() <= tol
