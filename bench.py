@@ -387,6 +387,42 @@ def streamed_launch_ms(torch, work, i, fwd, bwd, reps=20):
 L2_BYTES = 126 * 1024 * 1024
 
 
+def measure_window_copies(dev, reps=20):
+    """K3/K4 (window_partition / window_reverse with the Swin cyclic shift) at the stage-1
+    feature maps of Swin-T 224^2 B=128 and Swin-B 384^2 B=64: bytes moved = read + write of
+    the map; average of `reps` back-to-back launches (each > 2x L2 is not guaranteed here:
+    the maps are 77 / 151 MB, so the copy partly hits L2 -- reported as measured)."""
+    import torch
+
+    import paper_2501_06480_b200 as fwa
+    from paper_2501_06480_b200 import ops
+
+    peak, _ = load_peaks()
+    out = []
+    for (shape, k, shift) in (((128, 56, 56, 96), 7, 3), ((64, 96, 96, 128), 12, 6)):
+        x = fwa.fill_uniform(fwa.Rng(3), shape, dtype=torch.bfloat16, device=dev)
+        y = ops.window_partition(x, k, shift)
+        B, H, W, C = shape
+        for name, fn in (("partition", lambda: ops.window_partition(x, k, shift, )),
+                         ("reverse", lambda: ops.window_reverse(y, k, H, W, shift))):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            byts = 2 * x.numel() * x.element_size()
+            out.append({"op": name, "shape": list(shape), "window": k, "shift": shift,
+                        "dtype": "bf16", "ms": ms, "GB/s": byts / ms / 1e6,
+                        "frac": byts / ms / 1e6 / peak, "bytes": byts})
+        del x, y
+    return out
+
+
 def shard_workload(wl, rank, world):
     """Strong scaling: this rank's contiguous range of the workload's fixed global batch
     (shard.shard_images: whole images, so window n keeps its mask index n mod nW)."""
@@ -538,8 +574,9 @@ def run_gpu(args):
             embedded[name] = measure(args, name, dev, rank, world, dist,
                                      max(3, args.steps // 4), False)
     extra = embedded.get("swin_t_fwdbwd")
-    blocks = None
+    blocks = windows_k = None
     if args.workload == "swin_t_fwd" and not args.no_extra and world == 1:
+        windows_k = measure_window_copies(dev)
         # SURVEY 8(f)4 / PAPER.md:257-260: the whole (S)W-MSA block, fwd + bwd, on the package's
         # kernels vs the same block in plain PyTorch ops (same weights, bf16, eager)
         from paper_2501_06480_b200.swin import block_speedup
@@ -590,6 +627,8 @@ def run_gpu(args):
         }
         if validation is not None:
             line["validation"] = validation
+        if windows_k is not None:
+            line["window_partition"] = windows_k
         if blocks is not None:
             line["swin_block"] = {
                 "what": "Swin (S)W-MSA block forward + backward (partition + qkv Linear + window "

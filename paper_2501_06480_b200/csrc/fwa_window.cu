@@ -14,33 +14,56 @@
 namespace fwa {
 namespace {
 
+// One warp per (window, pixel row r of the window): the k pixels of that row are one
+// contiguous run on the window side and one (or, when the cyclic shift wraps, two) run(s)
+// on the image side, so the warp does the index math once (32-bit, per run) and its lanes
+// stream the run's 16-byte vectors coalesced. Each lane's (pixel, vector) position inside a
+// run is advanced incrementally (no division per vector).
 template <typename V>
-__global__ void window_copy_kernel(fwa_win_desc dsc, const uint8_t* __restrict__ in,
-                                   uint8_t* __restrict__ out, int reverse) {
-  const int64_t rowv = (int64_t)dsc.channels * dsc.elem_bytes / sizeof(V);  // vectors per pixel
-  const int k = dsc.window, H = dsc.height, W = dsc.width;
-  const int nWc = W / k;
-  const int64_t nW = (int64_t)(H / k) * nWc;
-  const int64_t pixels = dsc.batch * (int64_t)H * W;
-  const int64_t total = pixels * rowv;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = e / rowv;       // window-major pixel index
-    const int64_t c = e - p * rowv;
-    const int64_t win = p / (k * k);
-    const int l = (int)(p - win * k * k);
-    const int64_t b = win / nW;
-    const int64_t w = win - b * nW;
-    const int wr = (int)(w / nWc), wc = (int)(w - (int64_t)wr * nWc);
-    int y = wr * k + l / k + dsc.shift;
-    int x = wc * k + l % k + dsc.shift;
+__global__ void __launch_bounds__(256) window_copy_kernel(fwa_win_desc dsc, const V* __restrict__ in,
+                                                          V* __restrict__ out, int reverse, int rowv,
+                                                          int units) {
+  const int k = dsc.window, H = dsc.height, W = dsc.width, shift = dsc.shift;
+  const int nWc = W / k, nW = (H / k) * nWc, run = k * rowv;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  // lane's first vector: pixel pix0, vector c0 of that pixel
+  const int pix0 = lane / rowv, c0 = lane - (lane / rowv) * rowv;
+  for (int unit = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; unit < units; unit += nwarps) {
+    const int win = unit / k, r = unit - win * k;
+    const int b = win / nW, w = win - b * nW;
+    const int wr = w / nWc, wc = w - wr * nWc;
+    int y = wr * k + r + shift;
     if (y >= H) y -= H;
-    if (x >= W) x -= W;
-    const int64_t img = ((b * H + y) * W + x) * rowv + c;  // image-major index
-    const V* src = reinterpret_cast<const V*>(in);
-    V* dst = reinterpret_cast<V*>(out);
-    if (reverse) dst[img] = src[e];
-    else dst[e] = src[img];
+    const int x0 = wc * k + shift;
+    const int64_t img_row = ((int64_t)b * H + y) * W;   // pixel index of (b, y, 0)
+    const int64_t win_row = (int64_t)unit * k;          // window-major pixel of (win, r, 0)
+    int pix = pix0, c = c0;
+    // 4 vectors per lane in flight: all loads of a group before its stores
+    for (int v = lane; v < run; v += 4 * 32) {
+      int64_t src[4], dst[4];
+      V val[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        int x = x0 + pix;
+        if (x >= W) x -= W;
+        const int64_t img = (img_row + x) * rowv + c;
+        const int64_t wm = (win_row + pix) * rowv + c;
+        src[t] = reverse ? wm : img;
+        dst[t] = reverse ? img : wm;
+        c += 32;
+        while (c >= rowv) {
+          c -= rowv;
+          ++pix;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (v + 32 * t < run) val[t] = in[src[t]];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (v + 32 * t < run) out[dst[t]] = val[t];
+    }
   }
 }
 
@@ -62,26 +85,23 @@ int launch_window(const fwa_win_desc* d, const void* in, void* out, cudaStream_t
   const int64_t total_bytes = d->batch * (int64_t)d->height * d->width * row_bytes;
   if (total_bytes == 0) return FWA_OK;
   const int threads = 256;
-  auto blocks_for = [&](int64_t nvec) {
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((nvec + threads - 1) / threads,
-                                                            (int64_t)device_sm_count() * 32));
+  const int64_t units64 = d->batch * (int64_t)(d->height / d->window) * (d->width / d->window) * d->window;
+  if (units64 >= ((int64_t)1 << 31) || d->batch * (int64_t)d->height * d->width >= ((int64_t)1 << 31))
+    return fail(FWA_ERR_CAPACITY, "window partition: more than 2^31 pixels per call");
+  const int units = (int)units64;
+  // a persistent grid of 8 warps per CTA, up to 16 CTAs per SM
+  const unsigned grid = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>((units + 7) / 8, (int64_t)device_sm_count() * 16));
+  auto go = [&](auto vec) {
+    using V = decltype(vec);
+    const int rowv = (int)(row_bytes / sizeof(V));
+    window_copy_kernel<V><<<grid, threads, 0, s>>>(*d, (const V*)in, (V*)out, reverse, rowv, units);
   };
-  if (row_bytes % 16 == 0 && align % 16 == 0) {
-    window_copy_kernel<uint4><<<blocks_for(total_bytes / 16), threads, 0, s>>>(
-        *d, (const uint8_t*)in, (uint8_t*)out, reverse);
-  } else if (row_bytes % 8 == 0 && align % 8 == 0) {
-    window_copy_kernel<uint2><<<blocks_for(total_bytes / 8), threads, 0, s>>>(
-        *d, (const uint8_t*)in, (uint8_t*)out, reverse);
-  } else if (row_bytes % 4 == 0 && align % 4 == 0) {
-    window_copy_kernel<uint32_t><<<blocks_for(total_bytes / 4), threads, 0, s>>>(
-        *d, (const uint8_t*)in, (uint8_t*)out, reverse);
-  } else if (row_bytes % 2 == 0 && align % 2 == 0) {
-    window_copy_kernel<uint16_t><<<blocks_for(total_bytes / 2), threads, 0, s>>>(
-        *d, (const uint8_t*)in, (uint8_t*)out, reverse);
-  } else {
-    window_copy_kernel<uint8_t><<<blocks_for(total_bytes), threads, 0, s>>>(
-        *d, (const uint8_t*)in, (uint8_t*)out, reverse);
-  }
+  if (row_bytes % 16 == 0 && align % 16 == 0) go(uint4{});
+  else if (row_bytes % 8 == 0 && align % 8 == 0) go(uint2{});
+  else if (row_bytes % 4 == 0 && align % 4 == 0) go(uint32_t{});
+  else if (row_bytes % 2 == 0 && align % 2 == 0) go(uint16_t{});
+  else go(uint8_t{});
   count_launch();
   return check_cuda(cudaGetLastError(), "window_copy_kernel launch");
 }

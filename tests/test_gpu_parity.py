@@ -157,6 +157,28 @@ def test_window_partition_reverse_bitwise():
             assert torch.equal(back, x)
 
 
+def _torch_partition(x, k, s):
+    B, H, W, C = x.shape
+    if s:
+        x = torch.roll(x, (-s, -s), (1, 2))
+    return x.view(B, H // k, k, W // k, k, C).permute(0, 1, 3, 2, 4, 5).reshape(-1, k * k, C)
+
+
+@pytest.mark.parametrize("B,H,C,k,s,dt", [
+    (128, 56, 96, 7, 3, torch.bfloat16), (128, 28, 192, 7, 3, torch.float16),
+    (128, 7, 768, 7, 0, torch.float16), (64, 96, 128, 12, 6, torch.bfloat16),
+    (3, 20, 5, 4, 3, torch.uint8), (2, 14, 7, 7, 2, torch.float64), (5, 9, 33, 3, 2, torch.float16),
+])
+def test_window_partition_full_size_and_element_widths(B, H, C, k, s, dt):
+    # every vector width of the copy kernel (16 / 8 / 4 / 2 / 1-byte moves) and the Swin-T /
+    # Swin-B stage shapes at full batch, bitwise against the same permutation in torch
+    x = torch.randint(0, 255, (B, H, H, C), dtype=torch.uint8, device="cuda") if dt == torch.uint8 \
+        else fwa.fill_uniform(fwa.Rng(B + C), (B, H, H, C), dtype=dt if dt != torch.float64 else torch.float32).to(dt)
+    y = ops.window_partition(x, k, s)
+    assert torch.equal(y, _torch_partition(x, k, s))
+    assert torch.equal(ops.window_reverse(y, k, H, H, s), x)
+
+
 def test_window_api_matches_reference_index_map(golden):
     _, arrays = golden
     cfg = fwa.WindowConfig(4, 4, 1, 2)

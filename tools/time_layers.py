@@ -35,6 +35,17 @@ def timed(fn, reps=20):
     return e0.elapsed_time(e1) / reps * 1e3, host
 
 
+def window_case(name, shape, dt, k, shift, reverse):
+    B, H, W, C = shape
+    x = fwa.fill_uniform(fwa.Rng(3), shape, dtype=dt)
+    y = ops.window_partition(x, k, shift)
+    fn = (lambda: ops.window_reverse(y, k, H, W, shift)) if reverse \
+        else (lambda: ops.window_partition(x, k, shift))
+    us, host = timed(fn)
+    byts = 2 * x.numel() * x.element_size()
+    return {"case": name, "us": round(us, 1), "GB/s": round(byts / us / 1e3), "host_us": round(host, 1)}
+
+
 def case(name, shape, dt, bwd, bias, mask_nw, dbias, tokens=False):
     N, h, L, d = shape
     rng = fwa.Rng(7)
@@ -73,7 +84,17 @@ CASES = {
     "bwd_tok_dbias": (B1, torch.bfloat16, True, True, 0, True, True),
 }
 
+WINDOW_CASES = {
+    "partition": ((128, 56, 56, 96), torch.bfloat16, 7, 3, False),
+    "reverse": ((128, 56, 56, 96), torch.bfloat16, 7, 3, True),
+    "partition_b": ((64, 96, 96, 128), torch.bfloat16, 12, 6, False),
+    "reverse_b": ((64, 96, 96, 128), torch.bfloat16, 12, 6, True),
+}
+
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
     for n in names:
-        print(json.dumps(case(n, *CASES[n])), flush=True)
+        if n in WINDOW_CASES:
+            print(json.dumps(window_case(n, *WINDOW_CASES[n])), flush=True)
+        else:
+            print(json.dumps(case(n, *CASES[n])), flush=True)
