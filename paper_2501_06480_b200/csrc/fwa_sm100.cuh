@@ -163,6 +163,13 @@ __device__ __forceinline__ void red_add_v4_hint(float4* a, float4 v, uint64_t po
                : "memory");
 }
 
+// 8 halves (four f16x2) reduced into global memory, L2 priority hint
+__device__ __forceinline__ void red_add_v4_f16x2_hint(uint4* a, uint4 v, uint64_t policy) {
+  asm volatile("red.relaxed.gpu.global.add.noftz.L2::cache_hint.v4.f16x2 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(policy)
+               : "memory");
+}
+
 // ---- programmatic dependent launch ------------------------------------------
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() {

@@ -260,7 +260,8 @@ struct FlatBAdd {
   int heads;
   int n_w;
   float* ws;
-  int slice_heads;   // heads per CTA partial: [slice_heads][L][L] fp32 (see range_heads)
+  int slice_heads;   // heads per CTA partial: [slice_heads][L][L] (see range_heads)
+  int half_parts;    // partials in f16 (when fp32 slices of all CTAs would not fit in L2)
 };
 
 // pieces mode: Q, dO, dQ through per-segment boxes (fwa_flat.cuh)
@@ -347,8 +348,11 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   }
   if constexpr (DBIAS) {
     griddep_wait();   // the slice may still be read by the previous call's reduction
-    float4* z = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.slice_heads * L * L);
-    for (int i = threadIdx.x; i < add.slice_heads * L * L / 4; i += kBThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int eb = add.half_parts ? 2 : 4;
+    float4* z = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(add.ws) +
+                                          (size_t)blockIdx.x * add.slice_heads * L * L * eb);
+    for (int i = threadIdx.x; i < add.slice_heads * L * L * eb / 16; i += kBThreads)
+      z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   tc_fence_before();
   __syncthreads();
@@ -918,6 +922,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const float2 is2 = make_float2(is, is);
         const uint64_t rpol = policy_evict_last();   // 4.3 KB/row slices stay resident in L2
         float4* slice = reinterpret_cast<float4*>(add.ws + (size_t)blockIdx.x * add.slice_heads * L * L);
+        uint4* sliceh = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(add.ws) +
+                                                 (size_t)blockIdx.x * add.slice_heads * L * L);
         int h0, h1;
         range_heads(fm, ua, ub, h0, h1);
         (void)h1;
@@ -934,13 +940,35 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             } else {
               uh = u % add.heads;
             }
-            float4* wp = slice + ((uh - h0) * L + i) * (L / 4);
+            if (add.half_parts) {
+              // f16 partials (8 keys per vector reduction): the slices of stages with many
+              // heads stay in L2; a partial sums <= units-per-CTA / heads terms
+              uint4* wp = sliceh + ((uh - h0) * L + i) * (L / 8);
+#pragma unroll 2
+              for (int it = 0; it < (L / 8 + 3) / 4; ++it) {
+                const int c8 = it * 4 + (lane >> 3);   // 8-key column
+                if (c8 < L / 8) {
+                  const uint4 w = *reinterpret_cast<const uint4*>(sDS + patom_off(lr, c8 * 8));
+                  const uint32_t wi[4] = {w.x, w.y, w.z, w.w};
+                  uint32_t ho[4];
+#pragma unroll
+                  for (int t = 0; t < 4; ++t) {
+                    const float2 f = __fmul2_rn(bunpack2<T>(wi[t]), is2);
+                    __half2 h2 = __floats2half2_rn(f.x, f.y);
+                    ho[t] = *reinterpret_cast<uint32_t*>(&h2);
+                  }
+                  red_add_v4_f16x2_hint(wp + c8, make_uint4(ho[0], ho[1], ho[2], ho[3]), rpol);
+                }
+              }
+            } else {
+              float4* wp = slice + ((uh - h0) * L + i) * (L / 4);
 #pragma unroll 3
-            for (int it = 0; it < L / 16; ++it) {
-              const int c = it * 4 + (lane >> 3);   // 4-key column (float4 of the slice row)
-              const uint2 w = *reinterpret_cast<const uint2*>(sDS + patom_off(lr, c * 4) + (c & 1) * 8);
-              const float2 a = __fmul2_rn(bunpack2<T>(w.x), is2), e = __fmul2_rn(bunpack2<T>(w.y), is2);
-              red_add_v4_hint(wp + c, make_float4(a.x, a.y, e.x, e.y), rpol);
+              for (int it = 0; it < L / 16; ++it) {
+                const int c = it * 4 + (lane >> 3);   // 4-key column (float4 of the slice row)
+                const uint2 w = *reinterpret_cast<const uint2*>(sDS + patom_off(lr, c * 4) + (c & 1) * 8);
+                const float2 a = __fmul2_rn(bunpack2<T>(w.x), is2), e = __fmul2_rn(bunpack2<T>(w.y), is2);
+                red_add_v4_hint(wp + c, make_float4(a.x, a.y, e.x, e.y), rpol);
+              }
             }
           }
         }
@@ -957,7 +985,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 
 // dbias[h][i][j] = sum over the CTAs c whose unit range covers head h (ascending c) of
 // their partial ws[c][h - h0(c)][i][j]: fixed order, deterministic
-__global__ void bflat_dbias_reduce_kernel(const float* __restrict__ ws, int grid, int64_t n_units,
+template <typename P>
+__global__ void bflat_dbias_reduce_kernel(const P* __restrict__ ws, int grid, int64_t n_units,
                                           FlatMap fm, int slice_heads, int LL,
                                           float* __restrict__ dbias) {
   const int64_t n = (int64_t)fm.heads * LL;
@@ -968,7 +997,7 @@ __global__ void bflat_dbias_reduce_kernel(const float* __restrict__ ws, int grid
     for (int c = 0; c < grid; ++c) {
       int h0, h1;
       range_heads(fm, (int64_t)c * n_units / grid, (int64_t)(c + 1) * n_units / grid, h0, h1);
-      if (hd >= h0 && hd <= h1) acc += ws[((size_t)c * slice_heads + (hd - h0)) * LL + ij];
+      if (hd >= h0 && hd <= h1) acc += (float)ws[((size_t)c * slice_heads + (hd - h0)) * LL + ij];
     }
     dbias[e] = acc;
   }
@@ -1010,6 +1039,20 @@ FlatMap bflat_map(const Geom& g, bool want_db, bool tok) {
 
 int bflat_grid(const Geom& g) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g.units, device_sm_count()));
+}
+
+// f16 dBias partials when the fp32 ones of all CTAs would exceed half of L2 (Swin-B stages
+// 2-4: 98 / 196 / 392 MB fp32), so the slices stay resident while Q/K/V/dO stream through.
+// FWA_DBIAS_PARTS=f32 / f16 forces either.
+bool bflat_half_parts(const Geom& g, int grid, int slice_heads) {
+  static const int force = [] {
+    const char* e = getenv("FWA_DBIAS_PARTS");
+    if (!e) return 0;
+    return e[1] == '1' ? 1 : (e[1] == '3' ? -1 : 0);   // "f16" -> 1, "f32" -> -1
+  }();
+  if (force) return force > 0;
+  const int64_t l2 = device_l2_bytes() > 0 ? device_l2_bytes() : (int64_t)126 << 20;
+  return (int64_t)grid * slice_heads * g.L * g.L * 4 > l2 / 2;
 }
 
 int bflat_slice_heads(const FlatMap& fm, int64_t units, int grid) {
@@ -1088,13 +1131,16 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
       if ((rc = get_tokens_map(&m[9], dqkv + 2 * hdb, dtype, N, L, 3, g.heads, D, 16))) return rc;
       m[0] = m[3] = m[4] = m[5] = m[1];   // unused: Q / dO / dQ go through per-segment maps
     }
-    FlatBAdd fa{g.add_table, g.heads, g.add_nw, ws, 1};
+    FlatBAdd fa{g.add_table, g.heads, g.add_nw, ws, 1, 0};
     if (add) {
       if constexpr (D != 32) return fail(FWA_ERR_CAPACITY, "flat backward: bias/mask need d = 32");
       if (!fa.table) return fail(FWA_ERR_SHAPE, "flat backward: bias/mask given without the add table");
     }
     const int grid = bflat_grid(g);
-    if (want_db) fa.slice_heads = bflat_slice_heads(fm, g.units, grid);
+    if (want_db) {
+      fa.slice_heads = bflat_slice_heads(fm, g.units, grid);
+      fa.half_parts = bflat_half_parts(g, grid, fa.slice_heads) ? 1 : 0;
+    }
     if (!pc) {
       if ((rc = launch_bflat_kern<T, D, L, false>(g, m, fa, fm, NoRowMaps{}, add, want_db, grid, s))) return rc;
     } else {
@@ -1117,8 +1163,13 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
     if (want_db) {
       const int LL = L * L;
       const int64_t n = (int64_t)g.heads * LL;
-      bflat_dbias_reduce_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 8 * 148), 256, 0, s>>>(
-          ws, grid, g.units, fm, fa.slice_heads, LL, dbias);
+      const unsigned rgrid = (unsigned)std::min<int64_t>((n + 255) / 256, 8 * 148);
+      if (fa.half_parts)
+        bflat_dbias_reduce_kernel<__half><<<rgrid, 256, 0, s>>>(reinterpret_cast<const __half*>(ws), grid,
+                                                                 g.units, fm, fa.slice_heads, LL, dbias);
+      else
+        bflat_dbias_reduce_kernel<float><<<rgrid, 256, 0, s>>>(ws, grid, g.units, fm, fa.slice_heads, LL,
+                                                                dbias);
       if ((rc = check_cuda(cudaGetLastError(), "bflat_dbias_reduce_kernel launch"))) return rc;
       count_launch();
     }
@@ -1215,7 +1266,8 @@ size_t tc_bwd_flat_workspace_bytes(const Geom& g) {
   // dBias partials: [grid][slice_heads][L][L] fp32 (head-major walk: 1-2 heads per CTA)
   const int grid = bflat_grid(g);
   const FlatMap fm = bflat_map(g, true, false);
-  return (size_t)grid * bflat_slice_heads(fm, g.units, grid) * g.L * g.L * sizeof(float);
+  const int sh = bflat_slice_heads(fm, g.units, grid);
+  return (size_t)grid * sh * g.L * g.L * (bflat_half_parts(g, grid, sh) ? 2 : 4);
 }
 
 bool tc_bwd_flat_tokens_supported(const Geom& g, int dtype, bool has_bias, bool has_mask,

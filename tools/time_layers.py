@@ -17,6 +17,25 @@ import paper_2501_06480_b200 as fwa  # noqa: E402
 from paper_2501_06480_b200 import ops  # noqa: E402
 
 
+def timed_graph(fn, reps=20):
+    """Device us per call with `reps` calls captured in one CUDA graph (no host overhead)."""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3
+
+
 def timed(fn, reps=20):
     """(device us per call, host us per call): host >= device means the loop is launch-bound."""
     import time
@@ -76,6 +95,8 @@ CASES = {
     "fwd_bias_mask": (B1, torch.bfloat16, False, True, 64, False),
     "bwd": (B1, torch.float16, True, False, 0, False),
     "bwd_dbias": (B1, torch.bfloat16, True, True, 0, True),
+    "bwd_bias": (B1, torch.bfloat16, True, True, 0, False),
+    "bwd_bf16": (B1, torch.bfloat16, True, False, 0, False),
     "bwd_dbias_mask": (B1, torch.bfloat16, True, True, 64, True),
     "bwd_dbias_s3": (B3, torch.bfloat16, True, True, 4, True),
     "bwd_dbias_s4": (B4, torch.bfloat16, True, True, 0, True),
@@ -83,6 +104,34 @@ CASES = {
     "bwd_tok": (B1, torch.float16, True, False, 0, False, True),
     "bwd_tok_dbias": (B1, torch.bfloat16, True, True, 0, True, True),
 }
+
+# Swin-T stage layers, fwd fp16, timed inside a CUDA graph (the small ones are launch-bound
+# eagerly); each call on its own rotating buffers so consecutive calls do not hit in L2
+GRAPH_CASES = {"t0": (2, 3, 49, 32), "t00": (296, 3, 49, 32), "t1": (8192, 3, 49, 32), "t2": (2048, 6, 49, 32), "t3": (512, 12, 49, 32),
+               "t4": (128, 24, 49, 32), "b1": (4096, 4, 144, 32), "b3": (256, 16, 144, 32)}
+
+
+def graph_case(name, shape, bwd=False):
+    N, h, L, d = shape
+    rng = fwa.Rng(9)
+    nbuf = max(2, int(2 * 126e6 // (4 * N * h * L * d * 2)) + 1)
+    bufs = [tuple(fwa.fill_uniform(rng, shape, dtype=torch.float16) for _ in range(4)) for _ in range(nbuf)]
+    outs = [torch.empty_like(b[0]) for b in bufs]
+    it = [0]
+
+    def fn():
+        i = it[0] % nbuf
+        it[0] += 1
+        q, k, v, do = bufs[i]
+        if bwd:
+            ops.attention_backward(q, k, v, do, d ** -0.5)
+        else:
+            ops.attention_forward(q, k, v, d ** -0.5, out=outs[i])
+    us = timed_graph(fn, reps=6 * nbuf)
+    byts = (7 if bwd else 4) * N * h * L * d * 2
+    return {"case": name + ("_bwd" if bwd else ""), "us": round(us, 2), "GB/s": round(byts / us / 1e3),
+            "buffers": nbuf}
+
 
 WINDOW_CASES = {
     "partition": ((128, 56, 56, 96), torch.bfloat16, 7, 3, False),
@@ -94,7 +143,9 @@ WINDOW_CASES = {
 if __name__ == "__main__":
     names = sys.argv[1:] or list(CASES)
     for n in names:
-        if n in WINDOW_CASES:
+        if n.split("_")[0] in GRAPH_CASES:
+            print(json.dumps(graph_case(n.split("_")[0], GRAPH_CASES[n.split("_")[0]], n.endswith("_bwd"))), flush=True)
+        elif n in WINDOW_CASES:
             print(json.dumps(window_case(n, *WINDOW_CASES[n])), flush=True)
         else:
             print(json.dumps(case(n, *CASES[n])), flush=True)
