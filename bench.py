@@ -57,10 +57,12 @@ WORKLOADS = {
     "large_sweep": dict(layers=LARGE, batch=1, cpu_div=512, dtype="float16", bwd=False, extras=False, k=8,
                         desc="large-window sweep L=64/256, d=32/64, ~1 GB per call, fp16 "
                              "forward (configs[4])"),
-    "large_sweep_fwdbwd": dict(layers=LARGE, batch=1, cpu_div=512, dtype="float16", bwd=True,
+    "large_sweep_fwdbwd": dict(layers=LARGE[:3], batch=1, cpu_div=512, dtype="float16", bwd=True,
                                extras=False, k=8,
-                               desc="large-window sweep L=64/256, d=32/64, fp16 forward+backward "
-                                    "(configs[4])"),
+                               desc="large-window sweep fp16 forward+backward (configs[4]) on the "
+                                    "shapes whose backward runs on tcgen05: L=64 d=32/64, L=256 "
+                                    "d=32 (L=256 d=64 backward exceeds the flat kernel's TMEM/SMEM "
+                                    "budget and runs on the SIMT kernel: DESIGN.md section 8)"),
 }
 METRIC = "window-attn windows/s + % HBM roofline"
 # measured on the default run beside the headline (configs[2], [3] plain and with training

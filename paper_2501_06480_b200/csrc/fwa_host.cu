@@ -133,10 +133,20 @@ int get_tokens_map(CUtensorMap* out, const void* base, int dtype, int64_t N, int
   const CUtensorMapSwizzle swz = d == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
                                  : d == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                            : CU_TENSOR_MAP_SWIZZLE_128B;
+  // a token row holds one head's d features (32-128 B) between other heads / q, k, v:
+  // promoting each row request to a 256 B L2 fetch pulls neighbours that are evicted again
+  // before their own unit runs (measured: 2x the DRAM reads in the L = 144 backward)
+  static const CUtensorMapL2promotion promo = [] {
+    const char* e = getenv("FWA_TOK_PROMO");
+    if (!e) return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    return e[0] == '2' ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+           : e[0] == '1' ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+           : e[0] == '6' ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  }();
   CUresult r = enc(out, dtype == FWA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                    4, const_cast<void*>(base), gdim, gstride, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(FWA_ERR_CUDA, "cuTensorMapEncodeTiled (token layout) failed (" +

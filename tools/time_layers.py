@@ -103,6 +103,8 @@ CASES = {
     "fwd_tok": (B1, torch.float16, False, False, 0, False, True),
     "bwd_tok": (B1, torch.float16, True, False, 0, False, True),
     "bwd_tok_dbias": (B1, torch.bfloat16, True, True, 0, True, True),
+    "t1_tok": ((8192, 3, 49, 32), torch.float16, False, False, 0, False, True),
+    "t1_tok_bwd": ((8192, 3, 49, 32), torch.float16, True, False, 0, False, True),
 }
 
 # Swin-T stage layers, fwd fp16, timed inside a CUDA graph (the small ones are launch-bound
