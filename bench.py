@@ -486,6 +486,8 @@ def measure(args, name, dev, rank, world, dist, steps, with_e2e):
             "frac": kern[mk]["GB/s"] / peak,
             "traffic": ncu.get("dram_bytes_per_launch"),
             "traffic_source": ncu.get("source", "no committed ncu capture for this launch"),
+            "tensor_pipe_pct": ncu.get("tensor_pipe_pct"),
+            "issue_active_pct": ncu.get("issue_active_pct"),
             "peak_source": peak_src,
             "kernel": f"{mk} ({kern[mk]['kernel']}) on the dominant layer {kern[mk]['shape']}",
             "algorithmic_bytes_per_launch": mult * unit_bytes,
