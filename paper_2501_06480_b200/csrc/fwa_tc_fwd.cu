@@ -1,8 +1,9 @@
 // fwa_tc_fwd.cu — Flash Window Attention forward on tcgen05 + TMA (sm_100a).
 //
 // Algorithm 1 of the paper (reference flash.py:141-184) for
-// f16/bf16, L <= 64, d in {16, 32, 64}, without bias/mask (those shapes take
-// the generic kernel for now):
+// f16/bf16, L <= 64, d in {16, 32, 64}, optionally with the Swin relative-position
+// bias and shifted-window mask (ADD; fp32 rows kept in TMEM, see below), in the
+// [N][h][L][d] layout or straight from the packed qkv-Linear output (kTokens):
 //
 //   * A tile = 128 rows = two (window, head) units, each padded to 64 rows.
 //     TMA loads Q, K, V with a 3-D tensor map (d, L, units) and box (d, 64, 2):
