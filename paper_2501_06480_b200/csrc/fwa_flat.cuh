@@ -130,6 +130,28 @@ __device__ __forceinline__ void st_segments(const RowMaps& rm, const uint8_t* sr
   });
 }
 
+// Byte offset of row i of unit (n, hd): flat [units][L] rows or token-major rows of S x h
+// slots (the drain's direct global stores)
+template <int L>
+__device__ __forceinline__ int64_t unit_row_offset(const FlatMap& fm, int n, int hd, int i, int S,
+                                                   int row_bytes) {
+  if (fm.tok) return ((int64_t)(n * L + i) * S * fm.heads + hd) * row_bytes;
+  return ((int64_t)(n * fm.heads + hd) * L + i) * row_bytes;
+}
+
+// 16-byte global store, optionally with an L2 eviction-priority hint
+template <bool HINT>
+__device__ __forceinline__ void st_global_v4(void* p, uint4 v, uint64_t pol) {
+  if constexpr (HINT)
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                 : "memory");
+  else
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
 // Heads spanned by the virtual units [ua, ub) (their dBias partial slices)
 __host__ __device__ inline void range_heads(const FlatMap& fm, int64_t ua, int64_t ub, int& h0,
                                             int& h1) {

@@ -264,6 +264,15 @@ struct FlatBAdd {
   int half_parts;    // partials in f16 (when fp32 slices of all CTAs would not fit in L2)
 };
 
+// Gradient outputs for the drain's direct stores: base pointers (token-major: dq = dqkv and
+// dk / dv offset by h*d / 2*h*d elements) and the row pitch in slots (3 for dqkv, else 1)
+struct GradOut {
+  uint8_t* dq;
+  uint8_t* dk;
+  uint8_t* dv;
+  int S;
+};
+
 // pieces mode: Q, dO, dQ through per-segment boxes (fwa_flat.cuh)
 struct BwdPieceMaps {
   RowMaps q, dout, dq;
@@ -279,7 +288,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                 const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dk16,
                 const __grid_constant__ CUtensorMap tm_dv, const __grid_constant__ CUtensorMap tm_dv16,
                 int64_t n_units, float scale, FlatBAdd add, FlatMap fm,
-                const __grid_constant__ BwdPM<PC> pm) {
+                const __grid_constant__ BwdPM<PC> pm, GradOut go) {
   using C = BFCfg<D, L>;
   constexpr bool kBF16 = DT<T>::id == FWA_BF16;
   constexpr int QS = C::kQS, KS = C::kKS, VS = C::kVS, NKT = C::kNKT;
@@ -853,6 +862,30 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     };
     (void)emit_unit;
     (void)emit_block;
+    // Direct stores (default): each drain thread writes its own row straight from registers
+    // (rows are 32-128 contiguous bytes; a warp's 32 rows are contiguous in the flat layout),
+    // so emits need no staging buffer, no bulk-store wait and no drain-group barrier.
+    auto pack_row = [&](const uint32_t* x, int c) {
+      return make_uint4(bpack2<T>(__uint_as_float(x[8 * c]), __uint_as_float(x[8 * c + 1])),
+                        bpack2<T>(__uint_as_float(x[8 * c + 2]), __uint_as_float(x[8 * c + 3])),
+                        bpack2<T>(__uint_as_float(x[8 * c + 4]), __uint_as_float(x[8 * c + 5])),
+                        bpack2<T>(__uint_as_float(x[8 * c + 6]), __uint_as_float(x[8 * c + 7])));
+    };
+    auto put_row = [&](uint8_t* dst, const uint32_t* x) {
+      const uint64_t spol = DBIAS ? policy_evict_first() : 0;
+#pragma unroll
+      for (int c = 0; c < C::kChunks; ++c) st_global_v4<DBIAS>(dst + c * 16, pack_row(x, c), spol);
+    };
+    // row kt*128 + r of unit u (dK / dV)
+    auto put_unit_row = [&](uint8_t* base, const uint32_t* x, int u, int i) {
+      if constexpr (PC) {
+        int un, uh;
+        vunit_nh(fm, u, un, uh);
+        put_row(base + unit_row_offset<L>(fm, un, uh, i, go.S, C::kRowBytes), x);
+      } else {
+        put_row(base + ((int64_t)u * L + i) * C::kRowBytes, x);
+      }
+    };
     int n_unit = 0;
     for (int b = 0; b < nblk; ++b) {
       const int rs = r0 + b * kRows, re = min(rs + kRows, r1);
@@ -881,6 +914,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             mbar_arrive(&bars->acc_free);
           }
           const int nr = min(kRows, L - kt * kRows);
+#ifdef FWA_DRAIN_TMA
           if constexpr (PC) {
             int un, uh;
             vunit_nh(fm, u, un, uh);
@@ -890,6 +924,12 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             emit(gv, &tm_dv, &tm_dv16, u * L + kt * kRows, nr);
             emit(gk, &tm_dk, &tm_dk16, u * L + kt * kRows, nr);
           }
+#else
+          if (r < nr) {
+            put_unit_row(go.dv, gv, u, kt * kRows + r);
+            put_unit_row(go.dk, gk, u, kt * kRows + r);
+          }
+#endif
         }
         ++n_unit;
       }
@@ -905,8 +945,15 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bars->dq_free);
+#ifdef FWA_DRAIN_TMA
       if constexpr (PC) emit_block(gq, rs, re - rs);
       else emit(gq, &tm_dq, &tm_dq16, rs, re - rs);
+#else
+      if (r < re - rs) {
+        const int vr = rs + r, v = vr / L;
+        put_unit_row(go.dq, gq, v, vr - v * L);
+      }
+#endif
 #endif
       if (leader) BTRACE(7, b);
       if constexpr (DBIAS) {
@@ -1068,11 +1115,12 @@ int bflat_slice_heads(const FlatMap& fm, int64_t units, int grid) {
 template <bool PC>
 using BFlatKern = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
                            CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, int64_t, float, FlatBAdd,
-                           FlatMap, BwdPM<PC>);
+                           FlatMap, BwdPM<PC>, GradOut);
 
 template <typename T, int D, int L, bool PC>
 int launch_bflat_kern(const Geom& g, const CUtensorMap* m, const FlatBAdd& fa, const FlatMap& fm,
-                      const BwdPM<PC>& pm, bool add, bool want_db, int grid, cudaStream_t s) {
+                      const BwdPM<PC>& pm, const GradOut& go, bool add, bool want_db, int grid,
+                      cudaStream_t s) {
   using C = BFCfg<D, L>;
   // kernel variants: plain, + bias/mask, + bias/mask + dBias (bias/mask only for d = 32)
   BFlatKern<PC> kern = bwd_flat_kernel<T, D, L, false, false, PC>;
@@ -1083,7 +1131,7 @@ int launch_bflat_kern(const Geom& g, const CUtensorMap* m, const FlatBAdd& fa, c
   if ((rc = ensure_smem_attr((const void*)kern, (int)(C::kSmem), "cudaFuncSetAttribute(bwd_flat)"))) return rc;
   rc = check_cuda(launch_pdl(kern, dim3(grid), dim3(kBThreads), (size_t)C::kSmem, s, m[0], m[1], m[2],
                              m[3], m[4], m[5], m[6], m[7], m[8], m[9], (int64_t)g.units, g.scale, fa, fm,
-                             pm),
+                             pm, go),
                   "bwd_flat_kernel launch");
   if (rc) return rc;
   count_launch();
@@ -1136,13 +1184,20 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
       if constexpr (D != 32) return fail(FWA_ERR_CAPACITY, "flat backward: bias/mask need d = 32");
       if (!fa.table) return fail(FWA_ERR_SHAPE, "flat backward: bias/mask given without the add table");
     }
+    GradOut go;
+    if (fm.tok) {
+      uint8_t* base = static_cast<uint8_t*>(dq);
+      go = GradOut{base, base + hdb, base + 2 * hdb, 3};
+    } else {
+      go = GradOut{static_cast<uint8_t*>(dq), static_cast<uint8_t*>(dk), static_cast<uint8_t*>(dv), 1};
+    }
     const int grid = bflat_grid(g);
     if (want_db) {
       fa.slice_heads = bflat_slice_heads(fm, g.units, grid);
       fa.half_parts = bflat_half_parts(g, grid, fa.slice_heads) ? 1 : 0;
     }
     if (!pc) {
-      if ((rc = launch_bflat_kern<T, D, L, false>(g, m, fa, fm, NoRowMaps{}, add, want_db, grid, s))) return rc;
+      if ((rc = launch_bflat_kern<T, D, L, false>(g, m, fa, fm, NoRowMaps{}, go, add, want_db, grid, s))) return rc;
     } else {
       if constexpr (bflat_pc_built<D, L>()) {
         BwdPieceMaps pm;
@@ -1155,7 +1210,7 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
           if ((rc = get_row_maps(&pm.dout, dout, dtype, false, g.units, L, 1, 1, D))) return rc;
           if ((rc = get_row_maps(&pm.dq, dq, dtype, false, g.units, L, 1, 1, D))) return rc;
         }
-        if ((rc = launch_bflat_kern<T, D, L, true>(g, m, fa, fm, pm, add, want_db, grid, s))) return rc;
+        if ((rc = launch_bflat_kern<T, D, L, true>(g, m, fa, fm, pm, go, add, want_db, grid, s))) return rc;
       } else {
         return fail(FWA_ERR_CAPACITY, "flat backward: no pieces build for this shape");
       }
