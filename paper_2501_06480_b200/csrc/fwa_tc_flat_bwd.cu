@@ -533,8 +533,10 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const int rs = r0 + c * kRows, re = min(rs + kRows, r1);
         const int u0 = rs / L, u1 = (re - 1) / L;
         mbar_wait(&bars->p_ready, c & 1);
-        // (with kDSB = 1, ds_ready(c+1) needs ds_free(c), committed below: no phase aliasing)
-        mbar_wait(&bars->ds_ready, c & 1);
+        if constexpr (!C::kDV2) {
+          // (with kDSB = 1, ds_ready(c+1) needs ds_free(c), committed below: no phase aliasing)
+          mbar_wait(&bars->ds_ready, c & 1);
+        }
         MMA_FENCE_AFTER();
         if (lane == 0) BTRACE(1, c);
         const uint32_t q0 = smem_u32(sQD + qs * 2 * C::kTile), do0 = q0 + C::kTile;
@@ -560,8 +562,16 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           __syncwarp();
         };
         if constexpr (C::kDV2) {
-          // all dV first (a unit's two dV sets alternate by parity, no drain wait), so the
-          // softmax of c+1 may overwrite sP as early as possible
+          // all dV first, as soon as p and the 1/l-scaled dO are in smem (p_ready; dS is not
+          // needed), so sP is released for the softmax of c+1 while that of c still computes
+          // dS. A unit starting here reuses the dV set of the unit two before it: wait until
+          // the drain has read the last finished unit (drains run in unit order).
+          bool any_start = false;
+          for (int u = u0; u <= u1; ++u) any_start |= max(u * L, rs) == u * L;
+          if (any_start && n_done > 0) {
+            mbar_wait(&bars->acc_free, (n_done - 1) & 1);
+            MMA_FENCE_AFTER();
+          }
           for (int u = u0; u <= u1; ++u) {
             const int g_lo = max(u * L, rs), g_hi = min((u + 1) * L, re);
             const int k_lo = (g_lo - rs) / 16, k_hi = (g_hi - rs) / 16;
@@ -571,6 +581,9 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           __syncwarp();
           if (lane == 0) BTRACE(8, c);
           BPROBE(4, c);
+          // (with kDSB = 1, ds_ready(c+1) needs ds_free(c), committed below: no phase aliasing)
+          mbar_wait(&bars->ds_ready, c & 1);
+          MMA_FENCE_AFTER();
         }
         bool dq_issued = false;
         for (int u = u0; u <= u1; ++u) {
