@@ -217,3 +217,45 @@ def test_batched_contexts_carry_bias_and_mask_per_slice():
             c = ctxs[b][hd]
             assert torch.equal(c.q, q[b, hd]) and torch.equal(c.bias, bias[hd])
             assert torch.equal(c.mask, mask[b % nW]) and c.mask_windows == 1
+
+
+def _desc_v2(N, h, L, d, dtype=1, mask_windows=0, kernel=0):
+    return nat.FwaDesc(num_windows=N, heads=h, seq_len=L, head_dim=d, dtype=dtype, scale=0.2,
+                       chunks=1, mask_windows=mask_windows, kernel=kernel, reserved=0,
+                       add_table=None)
+
+
+def test_workspace_queries_size_the_add_table_and_partials_exactly():
+    # ABI 2: scratch is caller workspace; the library sizes it (no device work here)
+    lib = nat.load()
+    q = lambda f, *a: int(getattr(lib, f)(ctypes.byref(a[0]), *a[1:]))  # noqa: E731
+    # L <= 64 tile kernels read fp32 bias/mask directly: no table, no forward workspace
+    d49 = _desc_v2(64, 3, 49, 32, mask_windows=4)
+    assert q("fwa_add_table_bytes", d49, 1, 1) == 0
+    assert q("fwa_fwd_workspace_bytes", d49, 1, 1) == 0
+    # L = 144 flat kernels: f16 (bias + mask) * log2e table [n_w][h][L][L], 256-byte rounded
+    d144 = _desc_v2(256, 16, 144, 32, mask_windows=4)
+    tab = ((4 * 16 * 144 * 144 * 2 + 255) // 256) * 256
+    assert q("fwa_add_table_bytes", d144, 1, 1) == tab
+    assert q("fwa_fwd_workspace_bytes", d144, 1, 1) == tab
+    assert q("fwa_fwd_workspace_bytes", d144, 1, 0) == ((16 * 144 * 144 * 2 + 255) // 256) * 256
+    assert q("fwa_fwd_workspace_bytes", d144, 0, 0) == 0
+    # backward: table + per-CTA dBias partials (f16 here: fp32 slices would exceed L2 / 2)
+    ws = q("fwa_bwd_workspace_bytes", d144, 1, 1, 1)
+    assert ws > tab and (ws - tab) % (144 * 144 * 2) == 0
+    assert q("fwa_bwd_workspace_bytes", d144, 1, 1, 0) == tab
+    # a prebuilt table (desc.add_table) removes it from both queries
+    d144.add_table = 1 << 20
+    assert q("fwa_fwd_workspace_bytes", d144, 1, 1) == 0
+    assert q("fwa_bwd_workspace_bytes", d144, 1, 1, 1) == ws - tab
+
+
+def test_shard_fill_offsets_follow_the_counter_based_stream():
+    # fill_uniform_at(state, offset) must equal the slice of one fill_uniform draw: the
+    # per-rank shard of bench.py's validation (checked on the oracle's generator, no GPU)
+    from oracle import flashwin_oracle as orc
+
+    whole = orc.fill_uniform(orc.Rng(42), (10, 6))
+    state = 42 + 7 * 0x9E3779B97F4A7C15
+    part = orc.splitmix_u64(state & ((1 << 64) - 1), 12)
+    assert np.array_equal((part >> 11) * 2.0 ** -53 * 2.0 - 1.0, whole.reshape(-1)[7:19])
