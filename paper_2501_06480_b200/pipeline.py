@@ -24,6 +24,18 @@ def _chunk_bounds(n: int, period: int, chunks: int):
     return [(a, min(n, a + per)) for a in range(0, n, per)]
 
 
+def _n_chunks(t: torch.Tensor, requested) -> int:
+    """Chunks of ~CHUNK_BYTES per input tensor (the pipeline's fill + drain is one chunk of
+    H2D and one of D2H, so more chunks overlap more; each costs a few launches).
+    FWA_HOST_CHUNK_MB overrides the chunk size."""
+    if requested:
+        return requested
+    import os
+
+    mb = float(os.environ.get("FWA_HOST_CHUNK_MB", "8"))
+    return int(min(128, max(2, -(-t.numel() * t.element_size() // int(mb * (1 << 20))))))
+
+
 def _pinned(t: torch.Tensor) -> torch.Tensor:
     t = t.contiguous()
     return t if t.is_pinned() else t.pin_memory()
@@ -31,7 +43,7 @@ def _pinned(t: torch.Tensor) -> torch.Tensor:
 
 def host_forward(qh: torch.Tensor, kh: torch.Tensor, vh: torch.Tensor, scale: float,
                  bias: Optional[torch.Tensor] = None, mask: Optional[torch.Tensor] = None,
-                 chunks_r: int = 1, kernel: str = "auto", n_chunks: int = 8) -> torch.Tensor:
+                 chunks_r: int = 1, kernel: str = "auto", n_chunks: int = 0) -> torch.Tensor:
     """O for host (N, h, L, d) tensors; returns a pinned host tensor."""
     dev = torch.device("cuda", torch.cuda.current_device())
     qh, kh, vh = _pinned(qh), _pinned(kh), _pinned(vh)
@@ -47,7 +59,7 @@ def host_forward(qh: torch.Tensor, kh: torch.Tensor, vh: torch.Tensor, scale: fl
         t.record_stream(h2d)
     od.record_stream(d2h)
     nW = mask.shape[0] if mask is not None else 1
-    for a, b in _chunk_bounds(N, nW, n_chunks):
+    for a, b in _chunk_bounds(N, nW, _n_chunks(qh, n_chunks)):
         with torch.cuda.stream(h2d):
             for dst, src in ((qd, qh), (kd, kh), (vd, vh)):
                 dst[a:b].copy_(src[a:b], non_blocking=True)
@@ -66,7 +78,7 @@ def host_forward(qh: torch.Tensor, kh: torch.Tensor, vh: torch.Tensor, scale: fl
 
 
 def host_backward(qh, kh, vh, doh, scale: float, bias=None, mask=None, chunks_r: int = 1,
-                  kernel: str = "auto", want_dbias: bool = False, n_chunks: int = 8):
+                  kernel: str = "auto", want_dbias: bool = False, n_chunks: int = 0):
     """(dQ, dK, dV) pinned host tensors (+ dBias on the device, summed over chunks in order)."""
     dev = torch.device("cuda", torch.cuda.current_device())
     qh, kh, vh, doh = _pinned(qh), _pinned(kh), _pinned(vh), _pinned(doh)
@@ -81,7 +93,7 @@ def host_backward(qh, kh, vh, doh, scale: float, bias=None, mask=None, chunks_r:
         t.record_stream(h2d)
     nW = mask.shape[0] if mask is not None else 1
     dbias = None
-    for a, b in _chunk_bounds(N, nW, n_chunks):
+    for a, b in _chunk_bounds(N, nW, _n_chunks(qh, n_chunks)):
         with torch.cuda.stream(h2d):
             for dst, src in zip(ins_d, (qh, kh, vh, doh)):
                 dst[a:b].copy_(src[a:b], non_blocking=True)
