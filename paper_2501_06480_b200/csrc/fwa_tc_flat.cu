@@ -272,7 +272,9 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     // ===================== TMA producer =====================
     if (lane == 0 && nblk > 0) {
       griddep_wait();
-      const uint64_t pol = policy_evict_first();
+      // streamed once: evict_first -- except token-major rows (one head's 64 B of a 768 B
+      // token row), whose neighbours are the next units' rows: kept at normal priority
+      const uint64_t pol = (PC && fm.tok) ? policy_evict_normal() : policy_evict_first();
       int next = 0;  // next local unit to load
       const int n_loc = (int)(ub - ua);
       for (int b = 0; b < nblk; ++b) {
