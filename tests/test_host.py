@@ -259,3 +259,25 @@ def test_shard_fill_offsets_follow_the_counter_based_stream():
     state = 42 + 7 * 0x9E3779B97F4A7C15
     part = orc.splitmix_u64(state & ((1 << 64) - 1), 12)
     assert np.array_equal((part >> 11) * 2.0 ** -53 * 2.0 - 1.0, whole.reshape(-1)[7:19])
+
+
+def test_abi2_error_paths_fail_before_any_device_work():
+    # CAPACITY / SHAPE are raised by validation, before anything is enqueued (fake pointers
+    # are never dereferenced): the reference's "check before work" order (flash.py:156)
+    lib = nat.load()
+    before = lib.fwa_launch_count()
+    d = _desc_v2(64, 4, 144, 32)
+    fake = ctypes.c_void_p(0x1000)
+    # bias/mask on the large-window kernels without workspace for the add table
+    assert lib.fwa_fwd(ctypes.byref(d), fake, fake, fake, fake, None, fake, None, 0, None) == 2
+    assert b"workspace" in lib.fwa_last_error()
+    # a table needs a bias or a mask, and enough bytes
+    assert lib.fwa_build_add_table(ctypes.byref(d), None, None, fake, 1 << 30, None) == 1
+    assert lib.fwa_build_add_table(ctypes.byref(d), fake, None, fake, 16, None) == 2
+    # backward with dBias and a too-small workspace
+    n = int(lib.fwa_bwd_workspace_bytes(ctypes.byref(d), 1, 0, 1))
+    assert n > 0
+    st = lib.fwa_bwd(ctypes.byref(d), fake, fake, fake, fake, fake, None, fake, fake, fake, fake,
+                     fake, ctypes.c_size_t(n - 256), None)
+    assert st == 2
+    assert lib.fwa_launch_count() == before
