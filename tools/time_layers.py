@@ -110,7 +110,9 @@ CASES = {
 # Swin-T stage layers, fwd fp16, timed inside a CUDA graph (the small ones are launch-bound
 # eagerly); each call on its own rotating buffers so consecutive calls do not hit in L2
 GRAPH_CASES = {"t0": (2, 3, 49, 32), "t00": (296, 3, 49, 32), "t1": (8192, 3, 49, 32), "t2": (2048, 6, 49, 32), "t3": (512, 12, 49, 32),
-               "t4": (128, 24, 49, 32), "b1": (4096, 4, 144, 32), "b3": (256, 16, 144, 32)}
+               "t4": (128, 24, 49, 32), "b1": (4096, 4, 144, 32), "b3": (256, 16, 144, 32),
+               "l1": (61035, 1, 64, 32), "l2": (30517, 1, 64, 64), "l3": (15258, 1, 256, 32),
+               "l4": (7629, 1, 256, 64)}
 
 
 def graph_case(name, shape, bwd=False):
