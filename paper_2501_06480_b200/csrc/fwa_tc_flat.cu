@@ -572,17 +572,32 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 }
 
 // (bias[h] + mask[w]) * log2e -> f16 table [n_w][h][L][L] (either input may be null)
+// One (window, head) plane per blockIdx.y, 8 consecutive (i, j) per thread: two float4 of bias
+// and of mask in, one 16-byte f16 store out (L^2 % 8 == 0). No 64-bit division per element
+// (the grid-stride version took 32 us for a masked Swin-B stage-1 table).
 __global__ void flat_add_table_kernel(const float* __restrict__ bias, const float* __restrict__ mask,
                                       int heads, int n_w, int L, __half* __restrict__ out) {
-  const int64_t LL = (int64_t)L * L, n = (int64_t)n_w * heads * LL;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t ij = e % LL;
-    const int64_t h = (e / LL) % heads, w = e / (LL * heads);
-    float a = 0.f;
-    if (bias) a += bias[h * LL + ij];
-    if (mask) a += mask[w * LL + ij];
-    out[e] = __float2half_rn(a * 1.4426950408889634f);
+  const int LL = L * L, plane = blockIdx.y;   // plane = w * heads + h
+  const int h = plane % heads, w = plane / heads;
+  const float4* b4 = bias ? reinterpret_cast<const float4*>(bias + (size_t)h * LL) : nullptr;
+  const float4* m4 = mask ? reinterpret_cast<const float4*>(mask + (size_t)w * LL) : nullptr;
+  uint4* o = reinterpret_cast<uint4*>(out + (size_t)plane * LL);
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < LL / 8; v += gridDim.x * blockDim.x) {
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    if (b4) {
+      const float4 x = b4[2 * v], y = b4[2 * v + 1];
+      a0 = make_float4(a0.x + x.x, a0.y + x.y, a0.z + x.z, a0.w + x.w);
+      a1 = make_float4(a1.x + y.x, a1.y + y.y, a1.z + y.z, a1.w + y.w);
+    }
+    if (m4) {
+      const float4 x = m4[2 * v], y = m4[2 * v + 1];
+      a0 = make_float4(a0.x + x.x, a0.y + x.y, a0.z + x.z, a0.w + x.w);
+      a1 = make_float4(a1.x + y.x, a1.y + y.y, a1.z + y.z, a1.w + y.w);
+    }
+    const float k = 1.4426950408889634f;
+    __half2 r[4] = {__floats2half2_rn(a0.x * k, a0.y * k), __floats2half2_rn(a0.z * k, a0.w * k),
+                    __floats2half2_rn(a1.x * k, a1.y * k), __floats2half2_rn(a1.z * k, a1.w * k)};
+    o[v] = *reinterpret_cast<uint4*>(r);
   }
 }
 
@@ -745,8 +760,9 @@ int flat_build_add_table(const Geom& g, const float* bias, const float* mask, __
                          cudaStream_t s) {
   const int n_w = mask ? std::max(1, g.mask_windows) : 1;
   const int64_t n = (int64_t)n_w * g.heads * g.L * g.L;
-  flat_add_table_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, s>>>(
-      bias, mask, g.heads, n_w, g.L, out);
+  (void)n;
+  const int per_plane = (g.L * g.L / 8 + 255) / 256;
+  flat_add_table_kernel<<<dim3(per_plane, n_w * g.heads), 256, 0, s>>>(bias, mask, g.heads, n_w, g.L, out);
   int rc = check_cuda(cudaGetLastError(), "flat_add_table_kernel launch");
   if (rc) return rc;
   count_launch();
