@@ -460,22 +460,35 @@ bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ 
 // dbias[h][i][j] = sum over (CTA c, slot u) with (2c+u) % heads == h of ws[c][64u + i][j].
 // One warp per element: lane l sums c = l, l+32, ... in order, then a fixed shuffle tree —
 // the same order every run (deterministic, no atomics).
-// dbias[h][i][j] = sum over the tile slots t = 2c + u (CTA c, unit u) whose head is h, in
-// ascending t: fixed order, deterministic. One thread per (h, i, j) with j fastest, so a warp
-// reads a contiguous row segment of each slot's [64][64] partial (the warp-per-element version
-// gathered 4-byte words 32 KB apart: 12 us for 7 MB at Swin-T stage 1).
-__global__ void dbias_tc_reduce_kernel(const float* __restrict__ ws, int grid, int heads, int L,
-                                       float* __restrict__ dbias) {
+// dbias[h][i][j] = sum over the tile slots t = 2c + u (CTA c, unit u) whose head is h. A block
+// covers 32 consecutive (h, i, j) (threadIdx.x; j fastest, so a warp reads a contiguous row
+// segment of each slot's [64][64] partial) x 8 slot groups (threadIdx.y: group g takes the
+// head's slots g, g+8, g+16, ... in ascending order); the 8 group sums are then added in g
+// order -- a fixed association, so the result is deterministic. (A warp per element
+// gathering words 32 KB apart took 12 us for 7 MB at Swin-T stage 1.)
+__global__ void __launch_bounds__(256) dbias_tc_reduce_kernel(const float* __restrict__ ws, int grid,
+                                                              int heads, int L,
+                                                              float* __restrict__ dbias) {
+  __shared__ float part[8][33];
   const int n = heads * L * L;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+  const int e = blockIdx.x * 32 + threadIdx.x;
+  const int g = threadIdx.y;
+  float acc = 0.f;
+  if (e < n) {
     const int h = e / (L * L);
     const int r = e - h * L * L;
     const int i = r / L, j = r - (r / L) * L;
     const float* base = ws + (size_t)i * 64 + j;
-    float acc = 0.f;
 #pragma unroll 4
-    for (int t = h; t < 2 * grid; t += heads) acc += base[(size_t)t * 64 * 64];   // slot t = 2c + u
-    dbias[e] = acc;
+    for (int t = h + g * heads; t < 2 * grid; t += 8 * heads) acc += base[(size_t)t * 64 * 64];
+  }
+  part[g][threadIdx.x] = acc;
+  __syncthreads();
+  if (g == 0 && e < n) {
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum += part[k][threadIdx.x];
+    dbias[e] = sum;
   }
 }
 
@@ -533,7 +546,7 @@ int launch_bwd_t(const Geom& g, int dtype, const void* q, const void* k, const v
   count_launch();
   if (DBIAS) {
     const int n = g.heads * g.L * g.L;
-    dbias_tc_reduce_kernel<<<std::max(1, std::min((n + 127) / 128, 4096)), 128, 0, s>>>(
+    dbias_tc_reduce_kernel<<<(n + 31) / 32, dim3(32, 8), 0, s>>>(
         ws, grid, g.heads, g.L, dbias);
     count_launch();
     rc = check_cuda(cudaGetLastError(), "dbias_tc_reduce_kernel launch");
