@@ -961,55 +961,72 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// dbias[h][i][j] = sum over the CTAs c whose unit range covers head h (ascending c) of
-// their partial ws[c][h - h0(c)][i][j]: fixed order, deterministic. Each thread sums 16 bytes
-// of consecutive (i, j) per partial (8 f16 or 4 fp32 values): one vector load per CTA partial,
-// so the streaming read of the slices moves 16-byte requests (one-element threads issued 2-4
-// byte loads: 98 MB of f16 partials took 48 us at Swin-B stage 3). The unit-major walk covers
-// every head in every CTA (no range test in the loop).
+// dbias[h][i][j] = sum over the CTAs c whose unit range covers head h of their partial
+// ws[c][h - h0(c)][i][j], deterministic. A block covers 32 consecutive 16-byte vectors of the
+// output (threadIdx.x: 8 f16 or 4 fp32 partial values per load, contiguous across the warp) x
+// 8 CTA groups (threadIdx.y: group g sums CTAs g, g+8, ... in ascending order); the group
+// sums are added in g order -- a fixed association. (One thread per element issued 2-4 byte
+// loads and 148 dependent steps: 48 us for the 98 MB of f16 partials at Swin-B stage 3.)
 template <typename P>
-__global__ void bflat_dbias_reduce_kernel(const P* __restrict__ ws, int grid, int64_t n_units,
-                                          FlatMap fm, int slice_heads, int LL,
-                                          float* __restrict__ dbias) {
+__global__ void __launch_bounds__(256) bflat_dbias_reduce_kernel(const P* __restrict__ ws, int grid,
+                                                                 int64_t n_units, FlatMap fm,
+                                                                 int slice_heads, int LL,
+                                                                 float* __restrict__ dbias) {
   constexpr int V = 16 / sizeof(P);
+  __shared__ float part[8][32 * V + 1];
   const int LLv = LL / V;
   const int64_t nv = (int64_t)fm.heads * LLv;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nv;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int hd = (int)(e / LLv), ij = (int)(e - (int64_t)hd * LLv) * V;
-    float acc[V];
+  const int64_t e = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int g = threadIdx.y;
+  float acc[V];
 #pragma unroll
-    for (int t = 0; t < V; ++t) acc[t] = 0.f;
-    auto add = [&](int c, int h0) {
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(ws + ((size_t)c * slice_heads + (hd - h0)) * LL + ij));
-      if constexpr (sizeof(P) == 4) {
-        acc[0] += __uint_as_float(w.x);
-        acc[1] += __uint_as_float(w.y);
-        acc[2] += __uint_as_float(w.z);
-        acc[3] += __uint_as_float(w.w);
-      } else {
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ww[t]));
-          acc[2 * t] += f.x;
-          acc[2 * t + 1] += f.y;
-        }
-      }
-    };
-    if (!fm.head_major) {
-#pragma unroll 4
-      for (int c = 0; c < grid; ++c) add(c, 0);
+  for (int t = 0; t < V; ++t) acc[t] = 0.f;
+  const int hd = e < nv ? (int)(e / LLv) : 0;
+  const int ij = e < nv ? (int)(e - (int64_t)hd * LLv) * V : 0;
+  auto add = [&](int c, int h0) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(ws + ((size_t)c * slice_heads + (hd - h0)) * LL + ij));
+    if constexpr (sizeof(P) == 4) {
+      acc[0] += __uint_as_float(w.x);
+      acc[1] += __uint_as_float(w.y);
+      acc[2] += __uint_as_float(w.z);
+      acc[3] += __uint_as_float(w.w);
     } else {
-      for (int c = 0; c < grid; ++c) {
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ww[t]));
+        acc[2 * t] += f.x;
+        acc[2 * t + 1] += f.y;
+      }
+    }
+  };
+  if (e < nv) {
+    if (!fm.head_major) {   // every CTA covers every head: no range test in the loop
+#pragma unroll 4
+      for (int c = g; c < grid; c += 8) add(c, 0);
+    } else {
+      for (int c = g; c < grid; c += 8) {
         int h0, h1;
         range_heads(fm, (int64_t)c * n_units / grid, (int64_t)(c + 1) * n_units / grid, h0, h1);
         if (hd >= h0 && hd <= h1) add(c, h0);
       }
     }
-    float4* out = reinterpret_cast<float4*>(dbias + (size_t)hd * LL + ij);
+  }
 #pragma unroll
-    for (int t = 0; t < V / 4; ++t) out[t] = make_float4(acc[4 * t], acc[4 * t + 1], acc[4 * t + 2], acc[4 * t + 3]);
+  for (int t = 0; t < V; ++t) part[g][threadIdx.x * V + t] = acc[t];
+  __syncthreads();
+  if (g == 0 && e < nv) {
+    float out[V];
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += part[k][threadIdx.x * V + t];
+      out[t] = s;
+    }
+    float4* o = reinterpret_cast<float4*>(dbias + (size_t)hd * LL + ij);
+#pragma unroll
+    for (int t = 0; t < V / 4; ++t) o[t] = make_float4(out[4 * t], out[4 * t + 1], out[4 * t + 2], out[4 * t + 3]);
   }
 }
 
@@ -1182,12 +1199,12 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
       const int LL = L * L;
       const int64_t n = (int64_t)g.heads * LL;
       if (grid > 1024) return fail(FWA_ERR_CAPACITY, "flat backward: dBias reduce supports <= 1024 CTAs");
-      const unsigned rgrid = (unsigned)std::min<int64_t>((n / (fa.half_parts ? 8 : 4) + 127) / 128, 16 * 148);
+      const unsigned rgrid = (unsigned)((n / (fa.half_parts ? 8 : 4) + 31) / 32);
       if (fa.half_parts)
-        bflat_dbias_reduce_kernel<__half><<<rgrid, 128, 0, s>>>(reinterpret_cast<const __half*>(ws), grid,
+        bflat_dbias_reduce_kernel<__half><<<rgrid, dim3(32, 8), 0, s>>>(reinterpret_cast<const __half*>(ws), grid,
                                                                  g.units, fm, fa.slice_heads, LL, dbias);
       else
-        bflat_dbias_reduce_kernel<float><<<rgrid, 128, 0, s>>>(ws, grid, g.units, fm, fa.slice_heads, LL,
+        bflat_dbias_reduce_kernel<float><<<rgrid, dim3(32, 8), 0, s>>>(ws, grid, g.units, fm, fa.slice_heads, LL,
                                                                 dbias);
       if ((rc = check_cuda(cudaGetLastError(), "bflat_dbias_reduce_kernel launch"))) return rc;
       count_launch();
