@@ -262,6 +262,8 @@ struct FlatBAdd {
   float* ws;
   int slice_heads;   // heads per CTA partial: [slice_heads][L][L] (see range_heads)
   int half_parts;    // partials in f16 (when fp32 slices of all CTAs would not fit in L2)
+  int lazy_init;     // unit-major walk with >= heads units per CTA: the first unit of each head
+                     // stores its rows (initialising the slice), later units reduce into them
 };
 
 // Gradient outputs for the drain's direct stores: base pointers (token-major: dq = dqkv and
@@ -355,7 +357,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     const int lo = (t / 9) * 16, hi = (t % 9) * 16;
     lmtab[t] = make_uint4(blane_off(0, lo, hi), blane_off(1, lo, hi), blane_off(2, lo, hi), blane_off(3, lo, hi));
   }
-  if constexpr (DBIAS) {
+  if (DBIAS && !add.lazy_init) {
     griddep_wait();   // the slice may still be read by the previous call's reduction
     const int eb = add.half_parts ? 2 : 4;
     float4* z = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(add.ws) +
@@ -919,6 +921,10 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
             } else {
               uh = u % add.heads;
             }
+            // first unit of its head in this CTA: plain stores initialise the slice row (its
+            // rows precede every reduction into them in the walk; the producer's griddep_wait
+            // precedes all of this, so the previous call's reduce has finished reading)
+            const bool first = add.lazy_init && (u - (int)ua) < add.heads;
             if (add.half_parts) {
               // f16 partials (8 keys per vector reduction): the slices of stages with many
               // heads stay in L2; a partial sums <= units-per-CTA / heads terms
@@ -936,7 +942,8 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                     __half2 h2 = __floats2half2_rn(f.x, f.y);
                     ho[t] = *reinterpret_cast<uint32_t*>(&h2);
                   }
-                  red_add_v4_f16x2_hint(wp + c8, make_uint4(ho[0], ho[1], ho[2], ho[3]), rpol);
+                  if (first) st_global_v4<true>(wp + c8, make_uint4(ho[0], ho[1], ho[2], ho[3]), rpol);
+                  else red_add_v4_f16x2_hint(wp + c8, make_uint4(ho[0], ho[1], ho[2], ho[3]), rpol);
                 }
               }
             } else {
@@ -946,7 +953,11 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
                 const int c = it * 4 + (lane >> 3);   // 4-key column (float4 of the slice row)
                 const uint2 w = *reinterpret_cast<const uint2*>(sDS + patom_off(lr, c * 4) + (c & 1) * 8);
                 const float2 a = __fmul2_rn(bunpack2<T>(w.x), is2), e = __fmul2_rn(bunpack2<T>(w.y), is2);
-                red_add_v4_hint(wp + c, make_float4(a.x, a.y, e.x, e.y), rpol);
+                if (first)
+                  st_global_v4<true>(wp + c, make_uint4(__float_as_uint(a.x), __float_as_uint(a.y),
+                                                        __float_as_uint(e.x), __float_as_uint(e.y)), rpol);
+                else
+                  red_add_v4_hint(wp + c, make_float4(a.x, a.y, e.x, e.y), rpol);
               }
             }
           }
@@ -1082,6 +1093,15 @@ bool bflat_half_parts(const Geom& g, int grid, int slice_heads) {
   return (int64_t)grid * slice_heads * g.L * g.L * 4 > l2 / 2;
 }
 
+// FWA_DBIAS_ZERO=1: zero the partial slices up front instead of first-touch stores (A/B)
+bool bflat_eager_zero() {
+  static const bool on = [] {
+    const char* e = getenv("FWA_DBIAS_ZERO");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int bflat_slice_heads(const FlatMap& fm, int64_t units, int grid) {
   int sh = 1;
   for (int c = 0; c < grid; ++c) {
@@ -1159,7 +1179,7 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
       if ((rc = get_tokens_map(&m[9], dqkv + 2 * hdb, dtype, N, L, 3, g.heads, D, 16))) return rc;
       m[0] = m[3] = m[4] = m[5] = m[1];   // unused: Q / dO / dQ go through per-segment maps
     }
-    FlatBAdd fa{g.add_table, g.heads, g.add_nw, ws, 1, 0};
+    FlatBAdd fa{g.add_table, g.heads, g.add_nw, ws, 1, 0, 0};
     if (add) {
       if constexpr (D != 32) return fail(FWA_ERR_CAPACITY, "flat backward: bias/mask need d = 32");
       if (!fa.table) return fail(FWA_ERR_SHAPE, "flat backward: bias/mask given without the add table");
@@ -1175,6 +1195,8 @@ int launch_bflat_t(const Geom& g, int dtype, const void* q, const void* k, const
     if (want_db) {
       fa.slice_heads = bflat_slice_heads(fm, g.units, grid);
       fa.half_parts = bflat_half_parts(g, grid, fa.slice_heads) ? 1 : 0;
+      // every CTA's first `heads` units cover every (head, row) of its slice exactly once
+      fa.lazy_init = (!fm.head_major && g.units / grid >= g.heads && !bflat_eager_zero()) ? 1 : 0;
     }
     if (!pc) {
       if ((rc = launch_bflat_kern<T, D, L, false>(g, m, fa, fm, NoRowMaps{}, go, add, want_db, grid, s))) return rc;

@@ -154,3 +154,18 @@ def test_flat_backward_dbias_is_deterministic():
     bias = fwa.fill_uniform(rng, (4, 144, 144), -0.5, 0.5)
     outs = [ops.attention_backward(q, k, v, do, 0.2, bias, None, want_dbias=True)[3] for _ in range(6)]
     assert all(torch.equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("N,h", [(1024, 4), (256, 16)])
+def test_flat_backward_dbias_first_touch_partials_are_deterministic(N, h):
+    # >= heads units per CTA: each CTA's first unit of a head stores its partial rows, later
+    # units reduce into them (no up-front zeroing); fp32 and f16 partials
+    rng = fwa.Rng(N + h)
+    q, k, v, do = (fwa.fill_uniform(rng, (N, h, 144, 32), dtype=torch.bfloat16) for _ in range(4))
+    bias = fwa.fill_uniform(rng, (h, 144, 144), -1.0, 1.0)
+    outs = [ops.attention_backward(q, k, v, do, 0.2, bias, None, want_dbias=True)[3] for _ in range(4)]
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
+    bf = bias.clone().requires_grad_(True)
+    (torch.softmax((qf @ kf.transpose(-1, -2)) * 0.2 + bf[None], -1) @ vf).backward(do.float())
+    assert (outs[0] - bf.grad).abs().max().item() <= 2e-2 * max(1.0, bf.grad.abs().max().item())
