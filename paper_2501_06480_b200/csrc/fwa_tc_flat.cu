@@ -186,8 +186,8 @@ __device__ __forceinline__ void srow_stream_add(uint32_t taddr, const __half* ar
   };
   auto load = [&](int c, uint32_t (&r)[16], uint4 (&a)[2]) {
     tmem_ld16(taddr + c * 16, r);
-    a[0] = ldv4(arow + c * 16);
-    a[1] = ldv4(arow + c * 16 + 8);
+    a[0] = ldv4(arow + (2 * c) * (N * 8));       // chunk-major table: 8-column chunk k of
+    a[1] = ldv4(arow + (2 * c + 1) * (N * 8));   // row i at plane + (k * L + i) * 8
   };
   load(0, buf[0], ab[0]);
   tmem_wait_ld();
@@ -417,7 +417,7 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
           n = u / add.heads;
         }
         const int nw = n % add.n_w;
-        arow = add.table + ((int64_t)(nw * add.heads + hd) * L + i) * L;
+        arow = add.table + (int64_t)(nw * add.heads + hd) * L * L + i * 8;
       }
       // scores in the exp2 domain: s * scale * log2e (+ add)
       const float2 sc2 = make_float2(scale_log2, scale_log2);
@@ -572,31 +572,34 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
 }
 
 // (bias[h] + mask[w]) * log2e -> f16 table [n_w][h][L][L] (either input may be null)
-// One (window, head) plane per blockIdx.y, 8 consecutive (i, j) per thread: two float4 of bias
-// and of mask in, one 16-byte f16 store out (L^2 % 8 == 0). No 64-bit division per element
-// (the grid-stride version took 32 us for a masked Swin-B stage-1 table).
+// One (window, head) plane per blockIdx.y; thread v = (8-column chunk k, row i), i fastest:
+// the table is stored chunk-major, plane[k][i][8], so the softmax threads of a warp (32
+// consecutive rows) read one 512-byte run per 16-byte load instead of 32 rows 2L bytes apart
+// (that uncoalesced load was most of the bias cost of the forward: 230 vs 154 us).
 __global__ void flat_add_table_kernel(const float* __restrict__ bias, const float* __restrict__ mask,
                                       int heads, int n_w, int L, __half* __restrict__ out) {
   const int LL = L * L, plane = blockIdx.y;   // plane = w * heads + h
   const int h = plane % heads, w = plane / heads;
-  const float4* b4 = bias ? reinterpret_cast<const float4*>(bias + (size_t)h * LL) : nullptr;
-  const float4* m4 = mask ? reinterpret_cast<const float4*>(mask + (size_t)w * LL) : nullptr;
+  const float* bp = bias ? bias + (size_t)h * LL : nullptr;
+  const float* mp = mask ? mask + (size_t)w * LL : nullptr;
   uint4* o = reinterpret_cast<uint4*>(out + (size_t)plane * LL);
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < LL / 8; v += gridDim.x * blockDim.x) {
-    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-    if (b4) {
-      const float4 x = b4[2 * v], y = b4[2 * v + 1];
-      a0 = make_float4(a0.x + x.x, a0.y + x.y, a0.z + x.z, a0.w + x.w);
-      a1 = make_float4(a1.x + y.x, a1.y + y.y, a1.z + y.z, a1.w + y.w);
+    const int k = v / L, i = v - k * L;         // output (chunk k, row i)
+    const int src = i * L + k * 8;              // row-major (i, 8k .. 8k+7)
+    float a[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) a[t] = 0.f;
+    if (bp) {
+      const float4 x = *reinterpret_cast<const float4*>(bp + src), y = *reinterpret_cast<const float4*>(bp + src + 4);
+      a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w; a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
     }
-    if (m4) {
-      const float4 x = m4[2 * v], y = m4[2 * v + 1];
-      a0 = make_float4(a0.x + x.x, a0.y + x.y, a0.z + x.z, a0.w + x.w);
-      a1 = make_float4(a1.x + y.x, a1.y + y.y, a1.z + y.z, a1.w + y.w);
+    if (mp) {
+      const float4 x = *reinterpret_cast<const float4*>(mp + src), y = *reinterpret_cast<const float4*>(mp + src + 4);
+      a[0] += x.x; a[1] += x.y; a[2] += x.z; a[3] += x.w; a[4] += y.x; a[5] += y.y; a[6] += y.z; a[7] += y.w;
     }
-    const float k = 1.4426950408889634f;
-    __half2 r[4] = {__floats2half2_rn(a0.x * k, a0.y * k), __floats2half2_rn(a0.z * k, a0.w * k),
-                    __floats2half2_rn(a1.x * k, a1.y * k), __floats2half2_rn(a1.z * k, a1.w * k)};
+    const float kl = 1.4426950408889634f;
+    __half2 r[4] = {__floats2half2_rn(a[0] * kl, a[1] * kl), __floats2half2_rn(a[2] * kl, a[3] * kl),
+                    __floats2half2_rn(a[4] * kl, a[5] * kl), __floats2half2_rn(a[6] * kl, a[7] * kl)};
     o[v] = *reinterpret_cast<uint4*>(r);
   }
 }

@@ -669,10 +669,11 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       uint4 arow_half[ADD ? H / 8 : 1];
       if constexpr (ADD) {
         const int wrow = nrow % add.n_w;
+        // chunk-major table (fwa_tc_flat.cu): 8-column chunk k of row i at plane + (k*L + i)*8
         const uint4* ap = reinterpret_cast<const uint4*>(
-            add.table + ((int64_t)(wrow * add.heads + hrow) * L + irow) * L + hf * H);
+            add.table + (int64_t)(wrow * add.heads + hrow) * L * L + irow * 8) + hf * (H / 8) * L;
 #pragma unroll
-        for (int c = 0; c < H / 8; ++c) arow_half[c] = __ldg(ap + c);
+        for (int c = 0; c < H / 8; ++c) arow_half[c] = __ldg(ap + c * L);
       }
       mbar_wait(&bars->s_full, b & 1);
       tc_fence_after();
