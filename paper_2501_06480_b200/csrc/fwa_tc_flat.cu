@@ -167,34 +167,44 @@ struct FlatAdd {
   int n_w;
 };
 
-// srow_stream plus the matching 32 f16 of this row's add table: piece c+1's TMEM and L2
-// loads are both in flight while f(first column, scores, adds) runs on piece c.
+// volatile loads: kept in program order (plain __ldg gets hoisted for the whole row,
+// which spills at L >= 128)
+__device__ __forceinline__ uint4 ldv4_nc(const __half* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// srow_stream plus the matching 16 f16 of this row's add table per 16-column piece (two
+// 8-column chunks of the chunk-major table, coalesced across the warp). The first two pieces'
+// loads are issued by the caller before it waits for S (`pre`) and three pieces stay in
+// flight, so the L2 latency overlaps the barrier wait and the math of earlier pieces.
 template <int N, typename F>
-__device__ __forceinline__ void srow_stream_add(uint32_t taddr, const __half* arow, F&& f) {
-  // 16-column pieces (N % 16 == 0): 2 x (16 scores + 2 x 16 B of adds) in flight
+__device__ __forceinline__ void srow_stream_add(uint32_t taddr, const __half* arow,
+                                                const uint4 (&pre)[2][2], F&& f) {
   uint32_t buf[2][16];
-  uint4 ab[2][2];
+  uint4 ab[3][2];
   constexpr int kPieces = N / 16;
-  // volatile loads: kept in program order (plain __ldg gets hoisted for the whole row,
-  // which spills at L >= 128)
-  auto ldv4 = [](const __half* p) {
-    uint4 v;
-    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
-  };
-  auto load = [&](int c, uint32_t (&r)[16], uint4 (&a)[2]) {
-    tmem_ld16(taddr + c * 16, r);
-    a[0] = ldv4(arow + (2 * c) * (N * 8));       // chunk-major table: 8-column chunk k of
-    a[1] = ldv4(arow + (2 * c + 1) * (N * 8));   // row i at plane + (k * L + i) * 8
-  };
-  load(0, buf[0], ab[0]);
+  ab[0][0] = pre[0][0];
+  ab[0][1] = pre[0][1];
+  ab[1][0] = pre[1][0];
+  ab[1][1] = pre[1][1];
+  tmem_ld16(taddr, buf[0]);
+  if (kPieces > 2) {
+    ab[2][0] = ldv4_nc(arow + 4 * (N * 8));
+    ab[2][1] = ldv4_nc(arow + 5 * (N * 8));
+  }
   tmem_wait_ld();
 #pragma unroll
   for (int c = 0; c < kPieces; ++c) {
-    if (c + 1 < kPieces) load(c + 1, buf[(c + 1) & 1], ab[(c + 1) & 1]);
-    f(c * 16, buf[c & 1], ab[c & 1]);
+    if (c + 1 < kPieces) tmem_ld16(taddr + (c + 1) * 16, buf[(c + 1) & 1]);
+    f(c * 16, buf[c & 1], ab[c % 3]);
+    if (c + 3 < kPieces) {
+      ab[c % 3][0] = ldv4_nc(arow + (2 * (c + 3)) * (N * 8));
+      ab[c % 3][1] = ldv4_nc(arow + (2 * (c + 3) + 1) * (N * 8));
+    }
     tmem_wait_ld();
   }
 }
@@ -399,12 +409,11 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
       const int j = b % NB;
       const uint32_t tb = tmem + t_lane + s_col(b);
       const uint32_t tpw = tmem + t_lane + p_col(b);
-      mbar_wait(&bars->s_full[j], (b / NB) & 1);
-      tc_fence_after();
-      if (leader) FTRACE(3, b);
       float mx = -INFINITY;
-      // this row's (bias + mask) * log2e (f16, L2-resident table); rows past the range clamp
+      // this row's (bias + mask) * log2e (f16, L2-resident table); rows past the range clamp;
+      // its first pieces are requested before waiting for S
       const __half* arow = nullptr;
+      uint4 apre[2][2];
       if constexpr (ADD) {
         // 32-bit index math (rows < 2^31 is a precondition of the flat kernels)
         const int grow = min(r0 + b * kRows + r_in, r1 - 1);
@@ -418,13 +427,20 @@ fwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         }
         const int nw = n % add.n_w;
         arow = add.table + (int64_t)(nw * add.heads + hd) * L * L + i * 8;
+        apre[0][0] = ldv4_nc(arow);
+        apre[0][1] = ldv4_nc(arow + 1 * (L * 8));
+        apre[1][0] = ldv4_nc(arow + 2 * (L * 8));
+        apre[1][1] = ldv4_nc(arow + 3 * (L * 8));
       }
+      mbar_wait(&bars->s_full[j], (b / NB) & 1);
+      tc_fence_after();
+      if (leader) FTRACE(3, b);
       // scores in the exp2 domain: s * scale * log2e (+ add)
       const float2 sc2 = make_float2(scale_log2, scale_log2);
       if constexpr (ADD) {
         // pass 1 with the add row: x = s*scale*log2e + add is written back over S (TMEM) so
         // pass 2 reads it without touching the table again
-        srow_stream_add<L>(tb, arow, [&](int c0, const uint32_t* r, const uint4* a4) {
+        srow_stream_add<L>(tb, arow, apre, [&](int c0, const uint32_t* r, const uint4* a4) {
           uint32_t xs[16];
 #pragma unroll
           for (int t = 0; t < 16; t += 2) {
