@@ -99,6 +99,8 @@ CASES = {
     "bwd_bf16": (B1, torch.bfloat16, True, False, 0, False),
     "bwd_dbias_mask": (B1, torch.bfloat16, True, True, 64, True),
     "bwd_dbias_s3": (B3, torch.bfloat16, True, True, 4, True),
+    "bwd_bias_s3": (B3, torch.bfloat16, True, True, 4, False),
+    "bwd_s3": (B3, torch.bfloat16, True, False, 0, False),
     "bwd_dbias_s4": (B4, torch.bfloat16, True, True, 0, True),
     "fwd_tok": (B1, torch.float16, False, False, 0, False, True),
     "bwd_tok": (B1, torch.float16, True, False, 0, False, True),
