@@ -1017,11 +1017,13 @@ __global__ void __launch_bounds__(256) bflat_dbias_reduce_kernel(const P* __rest
 #pragma unroll 4
       for (int c = g; c < grid; c += 8) add(c, 0);
     } else {
-      for (int c = g; c < grid; c += 8) {
-        int h0, h1;
-        range_heads(fm, (int64_t)c * n_units / grid, (int64_t)(c + 1) * n_units / grid, h0, h1);
-        if (hd >= h0 && hd <= h1) add(c, h0);
-      }
+      // head-major: the CTAs covering head hd are the contiguous range [c_lo, c_hi]
+      // (ua(c) = floor(c U / G) < (hd + 1) N and ub(c) = floor((c + 1) U / G) > hd N)
+      const int64_t U = n_units, N = fm.n_win;
+      const int c_lo = (int)(((hd * N + 1) * grid + U - 1) / U) - 1;
+      const int c_hi = (int)((((int64_t)hd + 1) * N * grid + U - 1) / U) - 1;
+      for (int c = max(c_lo, 0) + g; c <= min(c_hi, grid - 1); c += 8)
+        add(c, (int)((int64_t)c * U / grid / N));
     }
   }
 #pragma unroll
@@ -1051,26 +1053,32 @@ constexpr bool bflat_pc_built() {
   return bflat_pc_built_rt(D, L);
 }
 
-// Walk order of a call: head-major when dBias is wanted and a 128-row block cannot hold two
-// rows of one (head, query) slot (L >= 128), so each CTA's partial covers 1-2 heads.
-// FWA_FLAT_WALK=head opts into the head-major dBias walk. Off by default: measured on B200
-// (tools/time_layers.py, Swin-B stage 3 (256,16,144,32) bf16 with dBias) 453 us head-major vs
-// 333 us unit-major -- the pieces addressing (two TMA boxes per 128-row block and tensor,
-// unit-dependent coordinates on the producer / drain threads) costs more than the L2-missing
-// partial slices it removes.
-bool bflat_head_walk() {
-  static const bool on = [] {
+// Walk order of a dBias call. Unit-major (the physical order, flat addressing) unless a CTA's
+// unit range is shorter than the head count: then every CTA would keep (and zero) a partial
+// for every head although it touches only a few, and the head-major walk (each CTA covers 1-2
+// heads: pieces addressing) wins. Measured on B200 (tools/time_layers.py, bf16, bias + dBias):
+// Swin-B stage 4 (64, 32, 144, 32) 180 -> 145 us head-major; stage 3 (256, 16, 144, 32) 224 us
+// unit-major vs 250 us head-major, stage 1 815 vs 870 us (the pieces addressing costs more
+// than the partial traffic it saves once a CTA spans all heads). Head-major needs a 128-row
+// block to hold at most one row per (head, query) slot (L >= 128). FWA_FLAT_WALK=head / unit
+// forces either.
+int bflat_walk_override() {
+  static const int v = [] {
     const char* e = getenv("FWA_FLAT_WALK");
-    return e && e[0] == 'h';
+    if (!e) return 0;
+    return e[0] == 'h' ? 1 : (e[0] == 'u' ? -1 : 0);
   }();
-  return on;
+  return v;
 }
+
+int bflat_grid(const Geom& g);
 
 FlatMap bflat_map(const Geom& g, bool want_db, bool tok) {
   FlatMap fm;
   fm.tok = tok ? 1 : 0;
-  fm.head_major = (want_db && g.L >= 128 && g.heads > 1 && bflat_pc_built_rt(g.d, g.L) &&
-                   bflat_head_walk()) ? 1 : 0;
+  const bool can = want_db && g.L >= 128 && g.heads > 1 && bflat_pc_built_rt(g.d, g.L);
+  const int ov = bflat_walk_override();
+  fm.head_major = (can && (ov > 0 || (ov == 0 && g.units / bflat_grid(g) < g.heads))) ? 1 : 0;
   fm.heads = g.heads;
   fm.n_win = (int)(g.units / g.heads);
   return fm;

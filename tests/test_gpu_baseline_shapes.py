@@ -185,36 +185,42 @@ def test_large_bias_magnitudes_stay_within_tolerance():
     assert (db - rb).abs().max().item() <= TOL * max(1.0, rb.abs().max().item())
 
 
-_HEAD_WALK_SCRIPT = r"""
+_WALK_SCRIPT = r"""
 import sys, torch
 sys.path.insert(0, sys.argv[1])
 import paper_2501_06480_b200 as fwa
 from paper_2501_06480_b200 import ops
-N, h, L, d = 256, 16, 144, 32
+N, h = int(sys.argv[2]), int(sys.argv[3])
+L, d = 144, 32
 rng = fwa.Rng(4)
 q, k, v, do = (fwa.fill_uniform(rng, (N, h, L, d), dtype=torch.bfloat16) for _ in range(4))
 bias = fwa.fill_uniform(rng, (h, L, L), -3.0, 3.0)
 dq, dk, dv, db = ops.attention_backward(q, k, v, do, d ** -0.5, bias, None, want_dbias=True)
+db2 = ops.attention_backward(q, k, v, do, d ** -0.5, bias, None, want_dbias=True)[3]
 qf, kf, vf = (t.float().requires_grad_(True) for t in (q, k, v))
 bf = bias.clone().requires_grad_(True)
 s = (qf @ kf.transpose(-1, -2)) * d ** -0.5 + bf[None]
 (torch.softmax(s, -1) @ vf).backward(do.float())
 err = max((a.float() - b).abs().max().item() for a, b in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)))
 db_err = (db - bf.grad).abs().max().item() / max(1.0, bf.grad.abs().max().item())
-assert fwa._native.device_flags() == 0
+assert fwa._native.device_flags() == 0 and torch.equal(db, db2)
 print(err, db_err)
 """
 
 
-def test_head_major_dbias_walk_opt_in():
-    # FWA_FLAT_WALK=head: each CTA walks 1-2 heads (pieces addressing), partials [2][L][L]
+@pytest.mark.parametrize("walk", ["head", "unit"])
+@pytest.mark.parametrize("N,h", [(256, 16), (64, 32)])
+def test_dbias_walks_both_ways(walk, N, h):
+    # FWA_FLAT_WALK forces the head-major walk (each CTA covers 1-2 heads, pieces addressing;
+    # the default when a CTA's range is shorter than the head count, e.g. Swin-B stage 4) or
+    # the unit-major one (flat addressing, per-CTA partials over all heads)
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, FWA_FLAT_WALK="head")
-    out = subprocess.run([sys.executable, "-c", _HEAD_WALK_SCRIPT, root], env=env, check=True,
-                         capture_output=True, text=True, timeout=300).stdout.split()
+    env = dict(os.environ, FWA_FLAT_WALK=walk)
+    out = subprocess.run([sys.executable, "-c", _WALK_SCRIPT, root, str(N), str(h)], env=env,
+                         check=True, capture_output=True, text=True, timeout=300).stdout.split()
     err, db_err = float(out[-2]), float(out[-1])
     assert err <= TOL and db_err <= TOL, (err, db_err)
