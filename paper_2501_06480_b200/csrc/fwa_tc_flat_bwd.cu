@@ -372,6 +372,62 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
   griddep_launch_dependents();
 
   if (warp == 0) {
+   if constexpr (PC) {
+    // ===================== TMA producer (pieces mode) =====================
+    // the whole warp runs the loop: lane 0 keeps the K/V ring and the barrier bookkeeping,
+    // lanes 0-3 issue the <= 4 per-segment Q / dO boxes of a block concurrently (one thread
+    // issuing them serially was measured as most of the pieces mode's overhead)
+    if (nblk > 0) {
+      griddep_wait();
+      const uint64_t pol = fm.tok ? policy_evict_normal() : policy_evict_first();
+      const int n_loc = (int)(ub - ua);
+      int next = 0;
+      for (int b = 0; b < nblk; ++b) {
+        const int rs = r0 + b * kRows;
+        const int last = (min(rs + kRows, r1) - 1) / L - (int)ua;
+        const int first = next;
+        if (lane == 0) {
+          for (; next <= last && next < n_loc; ++next) {   // K first: S(b) needs Q and K only
+            const int s = next % KS;
+            int un, uh;
+            vunit_nh(fm, (int)(ua + next), un, uh);
+            mbar_wait(&bars->k_empty[s], ((next / KS) & 1) ^ 1);
+            mbar_arrive_expect_tx(&bars->k_full[s], (C::kSplitKV ? 1 : 2) * C::kKVBytes);
+            ld_unit_rows<L>(sK + s * C::kKVSlot, &tm_k, &bars->k_full[s], fm, un, uh, 0, pol);
+            if constexpr (!C::kSplitKV)
+              ld_unit_rows<L>(sV + s * C::kKVSlot, &tm_v, &bars->k_full[s], fm, un, uh, 0, pol);
+          }
+        }
+        __syncwarp();
+        const int qs = b % QS;
+        const int nrows = min(rs + kRows, r1) - rs;
+        mbar_wait(&bars->qd_empty[qs], ((b / QS) & 1) ^ 1);
+        if (lane == 0) mbar_arrive_expect_tx(&bars->qd_full[qs], 2 * nrows * C::kRowBytes);
+        __syncwarp();
+        if (lane < 4) {   // lane = 2 * segment + tensor (0: Q, 1: dO)
+          const RowMaps& rm = (lane & 1) ? pm.dout : pm.q;
+          uint8_t* dst = sQD + qs * 2 * C::kTile + (lane & 1) * C::kTile;
+          int seg = 0;
+          for_segments<L>(fm, rs, nrows, [&](int n, int hd, int i, int off, int len) {
+            if (seg++ == (lane >> 1))
+              ld_unit_rows<L>(dst + off * C::kRowBytes, &rm.m[len / 16 - 1], &bars->qd_full[qs], fm, n, hd, i, pol);
+          });
+        }
+        __syncwarp();
+        if (lane == 0) {
+          for (int u = first; C::kSplitKV && u < next; ++u) {   // V free once dP of u's last block ran
+            const int s = u % VS;
+            int un, uh;
+            vunit_nh(fm, (int)(ua + u), un, uh);
+            mbar_wait(&bars->v_empty[s], ((u / VS) & 1) ^ 1);
+            mbar_arrive_expect_tx(&bars->v_full[s], C::kKVBytes);
+            ld_unit_rows<L>(sV + s * C::kKVSlot, &tm_v, &bars->v_full[s], fm, un, uh, 0, pol);
+          }
+        }
+        __syncwarp();
+      }
+    }
+   } else {
     // ===================== TMA producer =====================
     if (lane == 0 && nblk > 0) {
       griddep_wait();
@@ -427,6 +483,7 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         }
       }
     }
+   }
   } else if (warp == 1 || warp == 14) {
     // ===== MMA issuer: S(b), dP(b), then the gradients of block b-1 =====
     if (nblk > 0) {
