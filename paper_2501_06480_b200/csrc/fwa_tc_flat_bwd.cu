@@ -429,11 +429,11 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
     }
    } else {
     // ===================== TMA producer =====================
-    if (lane == 0 && nblk > 0) {
+    // warp-wide loop: lane 0 keeps the barrier bookkeeping; lanes 0 / 1 issue the K / V and
+    // Q / dO loads of a step concurrently
+    if (nblk > 0) {
       griddep_wait();
-      // streamed once: evict_first -- except token-major rows (one head's 64 B of a 768 B
-      // token row), whose neighbours are the next units' rows: kept at normal priority
-      const uint64_t pol = (PC && fm.tok) ? policy_evict_normal() : policy_evict_first();
+      const uint64_t pol = policy_evict_first();   // streamed once
       const int n_loc = (int)(ub - ua);
       int next = 0;
       for (int b = 0; b < nblk; ++b) {
@@ -443,44 +443,31 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         for (; next <= last && next < n_loc; ++next) {   // K first: S(b) needs Q and K only
           const int s = next % KS;
           mbar_wait(&bars->k_empty[s], ((next / KS) & 1) ^ 1);
-          mbar_arrive_expect_tx(&bars->k_full[s], (C::kSplitKV ? 1 : 2) * C::kKVBytes);
-          if constexpr (PC) {
-            int un, uh;
-            vunit_nh(fm, (int)(ua + next), un, uh);
-            ld_unit_rows<L>(sK + s * C::kKVSlot, &tm_k, &bars->k_full[s], fm, un, uh, 0, pol);
-            if constexpr (!C::kSplitKV)
-              ld_unit_rows<L>(sV + s * C::kKVSlot, &tm_v, &bars->k_full[s], fm, un, uh, 0, pol);
-          } else {
+          if (lane == 0) mbar_arrive_expect_tx(&bars->k_full[s], (C::kSplitKV ? 1 : 2) * C::kKVBytes);
+          __syncwarp();
+          if (lane == 0)
             tma_load_3d(sK + s * C::kKVSlot, &tm_k, &bars->k_full[s], 0, (int)((ua + next) * L), 0, pol);
-            if constexpr (!C::kSplitKV)   // one ring: V rides on K's barriers (measured faster)
-              tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->k_full[s], 0, (int)((ua + next) * L), 0, pol);
-          }
+          if (!C::kSplitKV && lane == 1)   // one ring: V rides on K's barriers (measured faster)
+            tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->k_full[s], 0, (int)((ua + next) * L), 0, pol);
+          __syncwarp();
         }
         const int qs = b % QS;
         mbar_wait(&bars->qd_empty[qs], ((b / QS) & 1) ^ 1);
-        if constexpr (PC) {   // rows not contiguous in memory: one box per unit segment
-          const int nrows = min(rs + kRows, r1) - rs;
-          mbar_arrive_expect_tx(&bars->qd_full[qs], 2 * nrows * C::kRowBytes);
-          ld_segments<L, C::kRowBytes>(sQD + qs * 2 * C::kTile, pm.q, &bars->qd_full[qs], fm, rs, nrows, pol);
-          ld_segments<L, C::kRowBytes>(sQD + qs * 2 * C::kTile + C::kTile, pm.dout, &bars->qd_full[qs], fm,
-                                       rs, nrows, pol);
-        } else {
-          mbar_arrive_expect_tx(&bars->qd_full[qs], 2 * C::kTile);
-          tma_load_3d(sQD + qs * 2 * C::kTile, &tm_q, &bars->qd_full[qs], 0, rs, 0, pol);
+        if (lane == 0) mbar_arrive_expect_tx(&bars->qd_full[qs], 2 * C::kTile);
+        __syncwarp();
+        if (lane == 0) tma_load_3d(sQD + qs * 2 * C::kTile, &tm_q, &bars->qd_full[qs], 0, rs, 0, pol);
+        if (lane == 1)
           tma_load_3d(sQD + qs * 2 * C::kTile + C::kTile, &tm_do, &bars->qd_full[qs], 0, rs, 0, pol);
-        }
-        for (int u = first; C::kSplitKV && u < next; ++u) {   // V free once dP of u's last block ran
-          const int s = u % VS;
-          mbar_wait(&bars->v_empty[s], ((u / VS) & 1) ^ 1);
-          mbar_arrive_expect_tx(&bars->v_full[s], C::kKVBytes);
-          if constexpr (PC) {
-            int un, uh;
-            vunit_nh(fm, (int)(ua + u), un, uh);
-            ld_unit_rows<L>(sV + s * C::kKVSlot, &tm_v, &bars->v_full[s], fm, un, uh, 0, pol);
-          } else {
+        __syncwarp();
+        if (lane == 0) {
+          for (int u = first; C::kSplitKV && u < next; ++u) {   // V free once dP of u's last block ran
+            const int s = u % VS;
+            mbar_wait(&bars->v_empty[s], ((u / VS) & 1) ^ 1);
+            mbar_arrive_expect_tx(&bars->v_full[s], C::kKVBytes);
             tma_load_3d(sV + s * C::kKVSlot, &tm_v, &bars->v_full[s], 0, (int)((ua + u) * L), 0, pol);
           }
         }
+        __syncwarp();
       }
     }
    }
