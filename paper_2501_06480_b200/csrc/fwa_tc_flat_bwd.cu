@@ -386,19 +386,19 @@ bwd_flat_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant_
         const int rs = r0 + b * kRows;
         const int last = (min(rs + kRows, r1) - 1) / L - (int)ua;
         const int first = next;
-        if (lane == 0) {
-          for (; next <= last && next < n_loc; ++next) {   // K first: S(b) needs Q and K only
-            const int s = next % KS;
+        for (; next <= last && next < n_loc; ++next) {   // K first: S(b) needs Q and K only
+          const int s = next % KS;
+          mbar_wait(&bars->k_empty[s], ((next / KS) & 1) ^ 1);
+          if (lane == 0) mbar_arrive_expect_tx(&bars->k_full[s], (C::kSplitKV ? 1 : 2) * C::kKVBytes);
+          __syncwarp();
+          if (lane < (C::kSplitKV ? 1 : 2)) {   // lane 0: K, lane 1: V (one ring)
             int un, uh;
             vunit_nh(fm, (int)(ua + next), un, uh);
-            mbar_wait(&bars->k_empty[s], ((next / KS) & 1) ^ 1);
-            mbar_arrive_expect_tx(&bars->k_full[s], (C::kSplitKV ? 1 : 2) * C::kKVBytes);
-            ld_unit_rows<L>(sK + s * C::kKVSlot, &tm_k, &bars->k_full[s], fm, un, uh, 0, pol);
-            if constexpr (!C::kSplitKV)
-              ld_unit_rows<L>(sV + s * C::kKVSlot, &tm_v, &bars->k_full[s], fm, un, uh, 0, pol);
+            ld_unit_rows<L>((lane ? sV : sK) + s * C::kKVSlot, lane ? &tm_v : &tm_k, &bars->k_full[s],
+                            fm, un, uh, 0, pol);
           }
+          __syncwarp();
         }
-        __syncwarp();
         const int qs = b % QS;
         const int nrows = min(rs + kRows, r1) - rs;
         mbar_wait(&bars->qd_empty[qs], ((b / QS) & 1) ^ 1);
