@@ -93,6 +93,7 @@ CASES = {
     "fwd": (B1, torch.float16, False, False, 0, False),
     "fwd_bias": (B1, torch.bfloat16, False, True, 0, False),
     "fwd_bias_mask": (B1, torch.bfloat16, False, True, 64, False),
+    "fwd_bias_s3": (B3, torch.bfloat16, False, True, 4, False),
     "bwd": (B1, torch.float16, True, False, 0, False),
     "bwd_dbias": (B1, torch.bfloat16, True, True, 0, True),
     "bwd_bias": (B1, torch.bfloat16, True, True, 0, False),
