@@ -99,6 +99,7 @@ CASES = {
     "bwd_bias": (B1, torch.bfloat16, True, True, 0, False),
     "bwd_bf16": (B1, torch.bfloat16, True, False, 0, False),
     "bwd_dbias_mask": (B1, torch.bfloat16, True, True, 64, True),
+    "bwd_dbias_s2": ((1024, 8, 144, 32), torch.bfloat16, True, True, 16, True),
     "bwd_dbias_s3": (B3, torch.bfloat16, True, True, 4, True),
     "bwd_bias_s3": (B3, torch.bfloat16, True, True, 4, False),
     "bwd_s3": (B3, torch.bfloat16, True, False, 0, False),
